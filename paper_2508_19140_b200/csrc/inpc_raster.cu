@@ -1,0 +1,602 @@
+// inpc_raster.cu — C ABI of the B200-native INPC rasterizer (include/inpc_raster.h).
+//
+// Host side: argument validation, the ctx's scratch arena and saved state,
+// and the stream-ordered launch sequence of the kernels in kernels.cuh.
+// Paper passages per step are cited in kernels.cuh and DESIGN.md §1.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "inpc_raster.h"
+#include "kernels.cuh"
+
+using namespace inpc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+enum Stage : int {
+  kStMemset = 0,
+  kStProject,
+  kStScan,
+  kStScatter,
+  kStSortBig,
+  kStBlendFwd,
+  kStBlendBwd,
+  kNumStages
+};
+const char* kStageNames[kNumStages] = {"memset", "project_count", "scan_tiles", "scatter",
+                                       "sort_big", "blend_fwd", "blend_bwd"};
+
+struct ViewState {
+  Buf ranges, sorted_idx, T_final, last, dbg_key, dbg_tiles, scalars;
+  uint64_t idx_cap = 0;
+};
+
+struct EventPair {
+  cudaEvent_t a, b;
+  int stage;
+};
+
+}  // namespace
+
+struct inpc_ctx {
+  int device = 0;
+  int num_sms = 148;
+  int big_grid = 0;
+  // scratch (shared by views, stream ordered)
+  Buf tile_count, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow;
+  uint64_t entry_cap = 0;
+  std::vector<ViewState> views;
+  // saved-state signature
+  bool have_state = false;
+  int32_t V = 0, H = 0, W = 0, C = 0, mode = 0, ty0 = 0, ty1 = 0;
+  int64_t N = 0;
+  unsigned flags = 0;
+  float sigma = 0, dil = 0, amax = 0, tmin = 0;
+  // profiling
+  bool profiling = false;
+  std::vector<EventPair> pending;
+  std::vector<cudaEvent_t> pool;
+  double stage_ms[kNumStages] = {};
+  int64_t stage_launches[kNumStages] = {};
+  cudaStream_t last_stream = nullptr;
+  uint32_t* host_scalars = nullptr;  // pinned
+};
+
+namespace {
+
+int fail_cuda(cudaError_t e, const char* what) {
+  char buf[256];
+  snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+  g_last_error = buf;
+  return INPC_CUDA;
+}
+
+#define CK(expr)                                   \
+  do {                                             \
+    cudaError_t e_ = (expr);                       \
+    if (e_ != cudaSuccess) return fail_cuda(e_, #expr); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Grow-only buffer.  Growing synchronises the stream first (the old buffer
+// may still be in use by enqueued work).
+int ensure(Buf& b, size_t bytes, cudaStream_t s) {
+  if (bytes <= b.bytes && b.p) return INPC_OK;
+  size_t nb = bytes < 256 ? 256 : bytes + bytes / 4;
+  if (b.p) {
+    cudaStreamSynchronize(s);
+    cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+  }
+  if (cudaMalloc(&b.p, nb) != cudaSuccess) {
+    cudaGetLastError();
+    g_last_error = "cudaMalloc failed";
+    return INPC_OOM;
+  }
+  b.bytes = nb;
+  return INPC_OK;
+}
+
+void free_buf(Buf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+cudaEvent_t get_event(inpc_ctx* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct StageTimer {
+  inpc_ctx* c;
+  cudaStream_t s;
+  EventPair ep{};
+  bool on;
+  StageTimer(inpc_ctx* ctx, cudaStream_t st, int stage, int launches) : c(ctx), s(st), on(ctx->profiling) {
+    c->stage_launches[stage] += launches;
+    if (!on) return;
+    ep.a = get_event(c);
+    ep.b = get_event(c);
+    ep.stage = stage;
+    cudaEventRecord(ep.a, s);
+  }
+  ~StageTimer() {
+    if (!on) return;
+    cudaEventRecord(ep.b, s);
+    c->pending.push_back(ep);
+  }
+};
+
+int validate_cfg(const inpc_raster_cfg* cfg, const inpc_camera* cams, int32_t V) {
+  if (!cfg || !cams || V <= 0) return INPC_INVALID_ARG;
+  if (cfg->H <= 0 || cfg->W <= 0 || cfg->H > 32768 || cfg->W > 32768) return INPC_INVALID_ARG;
+  if (cfg->C <= 0) return INPC_INVALID_ARG;
+  if (cfg->C > 64) return INPC_UNSUPPORTED;
+  if (cfg->splat_mode != INPC_SPLAT_BILINEAR && cfg->splat_mode != INPC_SPLAT_GAUSSIAN)
+    return INPC_INVALID_ARG;
+  if (!(cfg->alpha_max > 0.0f && cfg->alpha_max < 1.0f)) return INPC_INVALID_ARG;
+  if (!(cfg->t_min >= 0.0f && cfg->t_min < 1.0f)) return INPC_INVALID_ARG;
+  if (cfg->splat_mode == INPC_SPLAT_GAUSSIAN) {
+    if (!(cfg->dilation >= 0.0f) || !isfinite(cfg->dilation)) return INPC_INVALID_ARG;
+    if ((cfg->flags & INPC_FLAG_SIGMA_IS_PIXELS) && !(cfg->sigma > 0.0f)) return INPC_INVALID_ARG;
+  }
+  int tiles_y = (cfg->H + kTile - 1) / kTile;
+  if (!(cfg->tile_y_begin == 0 && cfg->tile_y_end == 0)) {
+    if (cfg->tile_y_begin < 0 || cfg->tile_y_end > tiles_y || cfg->tile_y_begin >= cfg->tile_y_end)
+      return INPC_INVALID_ARG;
+  }
+  for (int v = 0; v < V; ++v) {
+    const inpc_camera& c = cams[v];
+    if (!(c.fx > 0.0f && c.fy > 0.0f && c.z_near > 0.0f) || !isfinite(c.fx) || !isfinite(c.fy) ||
+        !isfinite(c.cx) || !isfinite(c.cy) || !isfinite(c.z_near))
+      return INPC_INVALID_ARG;
+  }
+  return INPC_OK;
+}
+
+void make_dev(const inpc_raster_cfg* cfg, const inpc_camera& cam, DevCam& dc, DevCfg& g) {
+  memcpy(dc.R, cam.R, sizeof dc.R);
+  memcpy(dc.t, cam.t, sizeof dc.t);
+  dc.fx = cam.fx;
+  dc.fy = cam.fy;
+  dc.cx = cam.cx;
+  dc.cy = cam.cy;
+  dc.z_near = cam.z_near;
+  g.H = cfg->H;
+  g.W = cfg->W;
+  g.C = cfg->C;
+  g.mode = cfg->splat_mode;
+  g.sigma = cfg->sigma;
+  g.dil = cfg->dilation;
+  g.amax = cfg->alpha_max;
+  g.tmin = cfg->t_min;
+  g.tiles_x = (cfg->W + kTile - 1) / kTile;
+  g.tiles_y = (cfg->H + kTile - 1) / kTile;
+  bool band = !(cfg->tile_y_begin == 0 && cfg->tile_y_end == 0);
+  g.ty0 = band ? cfg->tile_y_begin : 0;
+  g.ty1 = band ? cfg->tile_y_end : g.tiles_y;
+  g.flags = 0;
+  if (cfg->flags & INPC_FLAG_SIGMA_IS_PIXELS) g.flags |= kFlagSigmaPx;
+  if (cfg->flags & INPC_FLAG_SKIP_ZERO_ALPHA_GRAD) g.flags |= kFlagSkipZero;
+}
+
+int cmax_for(int C) { return C <= 4 ? 4 : C <= 8 ? 8 : C <= 16 ? 16 : C <= 32 ? 32 : 64; }
+
+template <int MODE, int CMAX>
+void launch_blend_fwd(int grid, cudaStream_t s, const DevCam& dc, const DevCfg& g, const float* xyz,
+                      const float* feat, const float* op, const float* bg, const uint32_t* ranges,
+                      const unsigned long long* entries, uint32_t* sorted_idx, const BlendOut& o) {
+  k_blend_fwd<MODE, CMAX><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, entries,
+                                                         sorted_idx, o);
+}
+
+template <int MODE>
+void dispatch_blend_fwd(int cmax, int grid, cudaStream_t s, const DevCam& dc, const DevCfg& g,
+                        const float* xyz, const float* feat, const float* op, const float* bg,
+                        const uint32_t* ranges, const unsigned long long* entries,
+                        uint32_t* sorted_idx, const BlendOut& o) {
+  switch (cmax) {
+    case 4: launch_blend_fwd<MODE, 4>(grid, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    case 8: launch_blend_fwd<MODE, 8>(grid, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    case 16: launch_blend_fwd<MODE, 16>(grid, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    case 32: launch_blend_fwd<MODE, 32>(grid, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    default: launch_blend_fwd<MODE, 64>(grid, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+  }
+}
+
+template <int MODE>
+void dispatch_blend_bwd(int cmax, int grid, cudaStream_t s, const DevCam& dc, const DevCfg& g,
+                        const float* xyz, const float* feat, const float* op, const float* bg,
+                        const uint32_t* ranges, const uint32_t* sorted_idx, const BwdIn& in) {
+  switch (cmax) {
+    case 4: k_blend_bwd<MODE, 4><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+    case 8: k_blend_bwd<MODE, 8><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+    case 16: k_blend_bwd<MODE, 16><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+    case 32: k_blend_bwd<MODE, 32><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+    default: k_blend_bwd<MODE, 64><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* inpc_version(void) { return "inpc_raster 0.1 sm_100a"; }
+
+const char* inpc_status_string(int status) {
+  switch (status) {
+    case INPC_OK: return "ok";
+    case INPC_INVALID_ARG: return "invalid argument";
+    case INPC_UNSUPPORTED: return "unsupported configuration";
+    case INPC_KEY_OVERFLOW: return "tile/entry count exceeds 32-bit indices";
+    case INPC_OOM: return "device allocation failed";
+    case INPC_CUDA: return g_last_error.empty() ? "CUDA error" : g_last_error.c_str();
+    case INPC_NO_STATE: return "backward without a matching forward on this context";
+    default: return "unknown status";
+  }
+}
+
+const char* inpc_stage_name(int32_t stage) {
+  return (stage >= 0 && stage < kNumStages) ? kStageNames[stage] : nullptr;
+}
+
+int inpc_ctx_create(inpc_ctx** out, int device) {
+  if (!out) return INPC_INVALID_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    g_last_error = "no such CUDA device";
+    return INPC_CUDA;
+  }
+  DeviceGuard dg(device);
+  inpc_ctx* c = new inpc_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_big, kBigThreads, 0);
+  c->big_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
+  if (cudaMallocHost(&c->host_scalars, 64) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return INPC_OOM;
+  }
+  *out = c;
+  return INPC_OK;
+}
+
+int inpc_ctx_destroy(inpc_ctx* c) {
+  if (!c) return INPC_INVALID_ARG;
+  DeviceGuard dg(c->device);
+  cudaDeviceSynchronize();
+  for (Buf* b : {&c->tile_count, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries,
+                 &c->tmp, &c->overflow})
+    free_buf(*b);
+  for (auto& v : c->views)
+    for (Buf* b : {&v.ranges, &v.sorted_idx, &v.T_final, &v.last, &v.dbg_key, &v.dbg_tiles, &v.scalars})
+      free_buf(*b);
+  for (auto& e : c->pending) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : c->pool) cudaEventDestroy(e);
+  if (c->host_scalars) cudaFreeHost(c->host_scalars);
+  delete c;
+  return INPC_OK;
+}
+
+int inpc_ctx_set_profiling(inpc_ctx* c, int enable) {
+  if (!c) return INPC_INVALID_ARG;
+  c->profiling = enable != 0;
+  return INPC_OK;
+}
+
+int inpc_ctx_stage_times(inpc_ctx* c, float* ms_out, int64_t* launches_out, int32_t n,
+                         int32_t* n_stages, int reset) {
+  if (!c) return INPC_INVALID_ARG;
+  DeviceGuard dg(c->device);
+  for (auto& e : c->pending) {
+    cudaEventSynchronize(e.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    c->stage_ms[e.stage] += ms;
+    c->pool.push_back(e.a);
+    c->pool.push_back(e.b);
+  }
+  c->pending.clear();
+  if (n_stages) *n_stages = kNumStages;
+  for (int k = 0; k < n && k < kNumStages; ++k) {
+    if (ms_out) ms_out[k] = (float)c->stage_ms[k];
+    if (launches_out) launches_out[k] = c->stage_launches[k];
+  }
+  if (reset) {
+    for (int k = 0; k < kNumStages; ++k) {
+      c->stage_ms[k] = 0;
+      c->stage_launches[k] = 0;
+    }
+  }
+  return INPC_OK;
+}
+
+int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camera* cams, int32_t V,
+                       const float* xyz, const float* feat, int64_t feat_view_stride,
+                       const float* opacity, int64_t N, const float* bg, int64_t bg_view_stride,
+                       float* out_feat, float* out_alpha, float* out_depth, int32_t* out_nfrag,
+                       int32_t* out_ncontrib, void* stream) {
+  if (!c) return INPC_INVALID_ARG;
+  int st = validate_cfg(cfg, cams, V);
+  if (st) return st;
+  if (N < 0 || N > 0xFFFFFFFFll) return N < 0 ? INPC_INVALID_ARG : INPC_KEY_OVERFLOW;
+  if (feat_view_stride != 0 && feat_view_stride != N * cfg->C) return INPC_INVALID_ARG;
+  const int64_t P = (int64_t)cfg->H * cfg->W;
+  if (bg_view_stride != 0 && bg_view_stride != P * cfg->C) return INPC_INVALID_ARG;
+  DeviceGuard dg(c->device);
+  if (N > 0 && (!is_device_ptr(xyz) || !is_device_ptr(feat) || !is_device_ptr(opacity)))
+    return INPC_INVALID_ARG;
+  if (!is_device_ptr(out_feat)) return INPC_INVALID_ARG;
+  if ((bg && !is_device_ptr(bg)) || (out_alpha && !is_device_ptr(out_alpha)) ||
+      (out_depth && !is_device_ptr(out_depth)) || (out_nfrag && !is_device_ptr(out_nfrag)) ||
+      (out_ncontrib && !is_device_ptr(out_ncontrib)))
+    return INPC_INVALID_ARG;
+  if (cfg->C == 4 && ((uintptr_t)feat % 16 || (uintptr_t)out_feat % 16 || (bg && (uintptr_t)bg % 16)))
+    return INPC_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  c->last_stream = s;
+  cudaGetLastError();
+
+  DevCam dc;
+  DevCfg g;
+  make_dev(cfg, cams[0], dc, g);
+  const int T = g.tiles_x * g.tiles_y;
+  const int band_tiles = (g.ty1 - g.ty0) * g.tiles_x;
+  const bool gauss = cfg->splat_mode == INPC_SPLAT_GAUSSIAN;
+  const bool debug = (cfg->flags & INPC_FLAG_DEBUG) != 0;
+  const int cmax = cmax_for(cfg->C);
+
+  // scratch
+  if ((st = ensure(c->tile_count, (size_t)(T + 1) * 4, s))) return st;
+  if ((st = ensure(c->cursor, (size_t)(T + 1) * 4, s))) return st;
+  if ((st = ensure(c->big_tiles, (size_t)(T + 1) * 4, s))) return st;
+  if ((st = ensure(c->big_elem, (size_t)(T + 2) * 4, s))) return st;
+  if ((st = ensure(c->big_chunk, (size_t)(T + 2) * 4, s))) return st;
+  if ((st = ensure(c->overflow, 64, s))) return st;
+  uint64_t bound = gauss ? 0 : 4ull * (uint64_t)N;  // bilinear: <= 4 tiles per point
+  if (!gauss && bound >= 0xFFFFFFFFull) return INPC_KEY_OVERFLOW;
+  if ((int)c->views.size() < V) c->views.resize(V);
+  c->have_state = false;
+
+  for (int v = 0; v < V; ++v) {
+    make_dev(cfg, cams[v], dc, g);
+    ViewState& vs = c->views[v];
+    if ((st = ensure(vs.ranges, (size_t)(T + 1) * 4, s))) return st;
+    if ((st = ensure(vs.T_final, (size_t)P * 4, s))) return st;
+    if ((st = ensure(vs.last, (size_t)P * 4, s))) return st;
+    if ((st = ensure(vs.scalars, sizeof(ViewScalars), s))) return st;
+    if (debug && N > 0) {
+      if ((st = ensure(vs.dbg_key, (size_t)N * 4, s))) return st;
+      if ((st = ensure(vs.dbg_tiles, (size_t)N * 4, s))) return st;
+    }
+    const float* feat_v = feat + (size_t)v * feat_view_stride;
+    const float* bg_v = bg ? bg + (size_t)v * bg_view_stride : nullptr;
+    uint32_t* tc = (uint32_t*)c->tile_count.p;
+    ViewScalars* sc = (ViewScalars*)vs.scalars.p;
+    {
+      StageTimer tm(c, s, kStMemset, 0);
+      CK(cudaMemsetAsync(tc, 0, (size_t)(T + 1) * 4, s));
+      CK(cudaMemsetAsync(c->overflow.p, 0, 4, s));
+    }
+    const int nblk = (int)((N + 255) / 256);
+    if (N > 0) {
+      StageTimer tm(c, s, kStProject, 1);
+      uint32_t* dk = debug ? (uint32_t*)vs.dbg_key.p : nullptr;
+      uint32_t* dt = debug ? (uint32_t*)vs.dbg_tiles.p : nullptr;
+      if (gauss) k_project_count<1><<<nblk, 256, 0, s>>>(dc, g, xyz, N, tc, dk, dt);
+      else k_project_count<0><<<nblk, 256, 0, s>>>(dc, g, xyz, N, tc, dk, dt);
+      CK(cudaGetLastError());
+    }
+    {
+      StageTimer tm(c, s, kStScan, 1);
+      k_scan_tiles<<<1, kScanThreads, 0, s>>>(T, tc, (uint32_t*)vs.ranges.p, (uint32_t*)c->cursor.p,
+                                             (uint32_t*)c->big_tiles.p, (uint32_t*)c->big_elem.p,
+                                             (uint32_t*)c->big_chunk.p, sc);
+      CK(cudaGetLastError());
+    }
+    uint64_t need = bound;
+    if (gauss) {
+      // the one data-dependent size: read F_t back (Gaussian footprints are unbounded)
+      CK(cudaMemcpyAsync(c->host_scalars, sc, sizeof(ViewScalars), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      need = c->host_scalars[0];
+      if (need >= 0xFFFFFFFFull) return INPC_KEY_OVERFLOW;
+    }
+    if ((st = ensure(c->entries, (size_t)(need ? need : 1) * 8, s))) return st;
+    if ((st = ensure(c->tmp, (size_t)(need ? need : 1) * 8, s))) return st;
+    if ((st = ensure(vs.sorted_idx, (size_t)(need ? need : 1) * 4, s))) return st;
+    vs.idx_cap = need;
+    if (N > 0) {
+      StageTimer tm(c, s, kStScatter, 1);
+      if (gauss)
+        k_scatter<1><<<nblk, 256, 0, s>>>(dc, g, xyz, N, (uint32_t*)c->cursor.p,
+                                          (unsigned long long*)c->entries.p, need,
+                                          (uint32_t*)c->overflow.p);
+      else
+        k_scatter<0><<<nblk, 256, 0, s>>>(dc, g, xyz, N, (uint32_t*)c->cursor.p,
+                                          (unsigned long long*)c->entries.p, need,
+                                          (uint32_t*)c->overflow.p);
+      CK(cudaGetLastError());
+    }
+    if (N > kSmemSortCap) {  // a tile can only exceed the SMEM cap with > cap points
+      StageTimer tm(c, s, kStSortBig, 1);
+      const uint32_t* r = (const uint32_t*)vs.ranges.p;
+      const uint32_t* bt = (const uint32_t*)c->big_tiles.p;
+      const uint32_t* be = (const uint32_t*)c->big_elem.p;
+      const uint32_t* bc = (const uint32_t*)c->big_chunk.p;
+      const ViewScalars* scc = sc;
+      unsigned long long* en = (unsigned long long*)c->entries.p;
+      unsigned long long* tp = (unsigned long long*)c->tmp.p;
+      uint32_t* si = (uint32_t*)vs.sorted_idx.p;
+      void* args[] = {(void*)&r, (void*)&bt, (void*)&be, (void*)&bc, (void*)&scc, (void*)&en, (void*)&tp, (void*)&si};
+      CK(cudaLaunchCooperativeKernel((void*)k_sort_big, c->big_grid, kBigThreads, args, 0, s));
+    }
+    {
+      StageTimer tm(c, s, kStBlendFwd, 1);
+      BlendOut o;
+      o.F = out_feat + (size_t)v * P * cfg->C;
+      o.A = out_alpha ? out_alpha + (size_t)v * P : nullptr;
+      o.D = out_depth ? out_depth + (size_t)v * P : nullptr;
+      o.nfrag = out_nfrag ? out_nfrag + (size_t)v * P : nullptr;
+      o.ncontrib = out_ncontrib ? out_ncontrib + (size_t)v * P : nullptr;
+      o.T_final = (float*)vs.T_final.p;
+      o.last = (uint32_t*)vs.last.p;
+      if (gauss)
+        dispatch_blend_fwd<1>(cmax, band_tiles, s, dc, g, xyz, feat_v, opacity, bg_v,
+                              (const uint32_t*)vs.ranges.p, (const unsigned long long*)c->entries.p,
+                              (uint32_t*)vs.sorted_idx.p, o);
+      else
+        dispatch_blend_fwd<0>(cmax, band_tiles, s, dc, g, xyz, feat_v, opacity, bg_v,
+                              (const uint32_t*)vs.ranges.p, (const unsigned long long*)c->entries.p,
+                              (uint32_t*)vs.sorted_idx.p, o);
+      CK(cudaGetLastError());
+    }
+  }
+  c->have_state = true;
+  c->V = V;
+  c->N = N;
+  c->H = cfg->H;
+  c->W = cfg->W;
+  c->C = cfg->C;
+  c->mode = cfg->splat_mode;
+  c->ty0 = g.ty0;
+  c->ty1 = g.ty1;
+  c->flags = cfg->flags;
+  c->sigma = cfg->sigma;
+  c->dil = cfg->dilation;
+  c->amax = cfg->alpha_max;
+  c->tmin = cfg->t_min;
+  return INPC_OK;
+}
+
+int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camera* cams, int32_t V,
+                       const float* xyz, const float* feat, int64_t feat_view_stride,
+                       const float* opacity, int64_t N, const float* bg, int64_t bg_view_stride,
+                       const float* g_feat, const float* g_alpha, const float* g_depth,
+                       float* g_point_feat, float* g_opacity, void* stream) {
+  if (!c) return INPC_INVALID_ARG;
+  int st = validate_cfg(cfg, cams, V);
+  if (st) return st;
+  if (N < 0) return INPC_INVALID_ARG;
+  if (feat_view_stride != 0 && feat_view_stride != N * cfg->C) return INPC_INVALID_ARG;
+  const int64_t P = (int64_t)cfg->H * cfg->W;
+  if (bg_view_stride != 0 && bg_view_stride != P * cfg->C) return INPC_INVALID_ARG;
+  DeviceGuard dg(c->device);
+  DevCam dc;
+  DevCfg g;
+  make_dev(cfg, cams[0], dc, g);
+  if (!c->have_state || c->V != V || c->N != N || c->H != cfg->H || c->W != cfg->W ||
+      c->C != cfg->C || c->mode != cfg->splat_mode || c->ty0 != g.ty0 || c->ty1 != g.ty1 ||
+      c->flags != cfg->flags || c->sigma != cfg->sigma || c->dil != cfg->dilation ||
+      c->amax != cfg->alpha_max || c->tmin != cfg->t_min)
+    return INPC_NO_STATE;
+  if (N > 0 && (!is_device_ptr(xyz) || !is_device_ptr(feat) || !is_device_ptr(opacity) ||
+                !is_device_ptr(g_point_feat) || !is_device_ptr(g_opacity)))
+    return INPC_INVALID_ARG;
+  if (!is_device_ptr(g_feat) || (g_alpha && !is_device_ptr(g_alpha)) ||
+      (g_depth && !is_device_ptr(g_depth)) || (bg && !is_device_ptr(bg)))
+    return INPC_INVALID_ARG;
+  if (cfg->C == 4 && ((uintptr_t)feat % 16 || (uintptr_t)g_feat % 16 ||
+                      (uintptr_t)g_point_feat % 16 || (bg && (uintptr_t)bg % 16)))
+    return INPC_INVALID_ARG;
+  if (N == 0) return INPC_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  c->last_stream = s;
+  cudaGetLastError();
+  const int band_tiles = (g.ty1 - g.ty0) * g.tiles_x;
+  const bool gauss = cfg->splat_mode == INPC_SPLAT_GAUSSIAN;
+  const int cmax = cmax_for(cfg->C);
+  for (int v = 0; v < V; ++v) {
+    make_dev(cfg, cams[v], dc, g);
+    ViewState& vs = c->views[v];
+    BwdIn in;
+    in.gF = g_feat + (size_t)v * P * cfg->C;
+    in.gA = g_alpha ? g_alpha + (size_t)v * P : nullptr;
+    in.gD = g_depth ? g_depth + (size_t)v * P : nullptr;
+    in.T_final = (const float*)vs.T_final.p;
+    in.last = (const uint32_t*)vs.last.p;
+    in.g_feat = g_point_feat + (size_t)v * feat_view_stride;
+    in.g_op = g_opacity;
+    const float* feat_v = feat + (size_t)v * feat_view_stride;
+    const float* bg_v = bg ? bg + (size_t)v * bg_view_stride : nullptr;
+    StageTimer tm(c, s, kStBlendBwd, 1);
+    if (gauss)
+      dispatch_blend_bwd<1>(cmax, band_tiles, s, dc, g, xyz, feat_v, opacity, bg_v,
+                            (const uint32_t*)vs.ranges.p, (const uint32_t*)vs.sorted_idx.p, in);
+    else
+      dispatch_blend_bwd<0>(cmax, band_tiles, s, dc, g, xyz, feat_v, opacity, bg_v,
+                            (const uint32_t*)vs.ranges.p, (const uint32_t*)vs.sorted_idx.p, in);
+    CK(cudaGetLastError());
+  }
+  return INPC_OK;
+}
+
+int inpc_debug_export(inpc_ctx* c, int32_t view, uint32_t* depth_keys, uint32_t* tiles_touched,
+                      uint32_t* tile_ranges, uint32_t* sorted_idx, int64_t sorted_cap,
+                      int64_t* F_t_out, void* stream) {
+  if (!c || !c->have_state || view < 0 || view >= c->V) return c ? INPC_NO_STATE : INPC_INVALID_ARG;
+  DeviceGuard dg(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  ViewState& vs = c->views[view];
+  const int T = ((c->W + kTile - 1) / kTile) * ((c->H + kTile - 1) / kTile);
+  CK(cudaMemcpyAsync(c->host_scalars, vs.scalars.p, sizeof(ViewScalars), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t Ft = c->host_scalars[0];
+  if (F_t_out) *F_t_out = Ft;
+  if ((depth_keys || tiles_touched) && !(c->flags & INPC_FLAG_DEBUG)) return INPC_INVALID_ARG;
+  if (depth_keys && c->N) CK(cudaMemcpyAsync(depth_keys, vs.dbg_key.p, (size_t)c->N * 4, cudaMemcpyDeviceToDevice, s));
+  if (tiles_touched && c->N) CK(cudaMemcpyAsync(tiles_touched, vs.dbg_tiles.p, (size_t)c->N * 4, cudaMemcpyDeviceToDevice, s));
+  if (tile_ranges) CK(cudaMemcpyAsync(tile_ranges, vs.ranges.p, (size_t)(T + 1) * 4, cudaMemcpyDeviceToDevice, s));
+  if (sorted_idx) {
+    int64_t n = Ft < sorted_cap ? Ft : sorted_cap;
+    if (n > 0) CK(cudaMemcpyAsync(sorted_idx, vs.sorted_idx.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  return INPC_OK;
+}
+
+}  // extern "C"
