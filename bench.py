@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Benchmark of the INPC neural point rasterizer (BASELINE.json metric:
+frames/s and Mpoints/s at 1080p fwd+bwd, % of B200 HBM roofline, 1/2/4/8 GPUs).
+
+One step = one pass of the whole hot path (H1-H8) over one
+synthetic frame: forward (project, tile lists, blend) + backward, with the
+point cloud and upstream gradients resident in HBM.  Default workload =
+config 2 (configs[1]: 2^20-point view-specific cloud, 1920x1080, bilinear,
+fwd+bwd).  Under torchrun (N > 1) every rank renders its own view-specific
+cloud (independent problems, no data-path collective): weak scaling.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the CPU oracle (oracle/, the only reference this
+paper-only build has) on the host cores, on a bounded sample of the same
+workload, and prints the same JSON line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synthgen  # noqa: E402
+
+METRIC = "frames/s and Mpoints/s at 1080p fwd+bwd, % of B200 HBM roofline, 1/2/4/8 GPUs"
+WORKLOAD = "cfg2: 2^20-point view-specific cloud, 1920x1080, C=4, bilinear 2x2 splats, fwd+bwd"
+NOMINAL_HBM_GBS = 8000.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ byte model
+def algorithmic_bytes(N, Nv, Ft, P, C):
+    """Compulsory bytes per stage: each datum the method must
+    move, counted once, whatever the implementation re-reads."""
+    return {
+        "project_count": 12 * N,                       # positions
+        "scan_tiles": 0,
+        "scatter": 8 * Ft,                             # one write of the (key, idx) record
+        "sort_big": 0,
+        "blend_fwd": 8 * Ft + (4 + 4 * C) * Nv + 4 * P * (C + 2) + 8 * P,
+        #            record read, opacity+features, F/A/D write, T_final+last write
+        "blend_bwd": 4 * P * (C + 2) + 8 * P + 4 * Ft + (16 + 4 * C) * Nv + 4 * (C + 1) * Nv,
+        #            upstream grads, saved state, sorted idx, xyz/o/f, gradient write
+    }
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def oracle_step(c, gF, gA, gD, frac, threads):
+    """Oracle fwd+bwd on a band of pixel rows covering `frac` of the frame."""
+    import oracle
+    H, W = c["H"], c["W"]
+    rows = max(1, int(round(frac * H)))
+    mask = np.zeros((H, W), np.uint8)
+    mask[:rows] = 1
+    t0 = time.perf_counter()
+    oracle.render(c["cams"][0], c["xyz"], c["feat"], c["opacity"], H, W, pixel_mask=mask,
+                  threads=threads)
+    oracle.backward(c["cams"][0], c["xyz"], c["feat"], c["opacity"], H, W, gF, gA, gD,
+                    pixel_mask=mask, threads=threads)
+    return time.perf_counter() - t0, rows / H
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    c = synthgen.config2()
+    H, W, C = c["H"], c["W"], c["C"]
+    gF, gA, gD = (x[0] for x in synthgen.upstream_grads(2, 1, H, W, C))
+    th = cpu_threads()
+    # size the per-step sample so the whole run stays within ~2 minutes
+    t_cal, f_cal = oracle_step(c, gF, gA, gD, 0.05, th)
+    per_frame = t_cal / f_cal
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    frac = float(min(1.0, max(0.01, budget / per_frame)))
+    for _ in range(args.warmup):
+        oracle_step(c, gF, gA, gD, frac, th)
+    tt, ff = 0.0, 0.0
+    for _ in range(args.steps):
+        t, f = oracle_step(c, gF, gA, gD, frac, th)
+        tt += t
+        ff += f
+    fps = ff / tt
+    N = c["xyz"].shape[0]
+    sample = f"{ff:.3f} frames ({args.steps} steps x {frac:.3f} of the 1080p rows) of cfg2 fwd+bwd"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "N": N, "H": H, "W": W, "C": C},
+        "mpoints_per_s": fps * N / 1e6,
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": th, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_19140_b200 as inpc
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    c = synthgen.config2(seed=2 + rank)
+    H, W, C = c["H"], c["W"], c["C"]
+    N = c["xyz"].shape[0]
+    P = H * W
+    xyz_h = torch.from_numpy(c["xyz"]).pin_memory()
+    feat_h = torch.from_numpy(c["feat"]).pin_memory()
+    op_h = torch.from_numpy(c["opacity"]).pin_memory()
+    gF_h, gA_h, gD_h = (torch.from_numpy(x).pin_memory() for x in synthgen.upstream_grads(2 + rank, 1, H, W, C))
+    xyz, feat, op = xyz_h.to(dev), feat_h.to(dev), op_h.to(dev)
+    gF, gA, gD = gF_h.to(dev), gA_h.to(dev), gD_h.to(dev)
+    ctx = inpc.Context(local_rank)
+    cfg = inpc.make_cfg(H, W, C, "bilinear")
+    cams = c["cams"]
+    out = dict(F=torch.empty((1, H, W, C), device=dev), A=torch.empty((1, H, W), device=dev),
+               D=torch.empty((1, H, W), device=dev))
+    g_feat = torch.zeros_like(feat)
+    g_op = torch.zeros_like(op)
+
+    def step():
+        g_feat.zero_()
+        g_op.zero_()
+        ctx.forward(cfg, cams, xyz, feat, op, out=out)
+        ctx.backward(cfg, cams, xyz, feat, op, gF, gA, gD, g_feat=g_feat, g_opacity=g_op)
+
+    # workload statistics (untimed): visible points, tile entries
+    dbg = inpc.make_cfg(H, W, C, "bilinear", flags=inpc.FLAG_DEBUG)
+    ctx.forward(dbg, cams, xyz, feat, op)
+    ex = ctx.debug_export(0, N=N, H=H, W=W)
+    Nv = int((ex["tiles_touched"] > 0).sum().item())
+    Ft = int(ex["F_t"])
+    model = algorithmic_bytes(N, Nv, Ft, P, C)
+    step_bytes = sum(model.values())
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    for _ in range(args.warmup):
+        step()
+    # clock ramp: keep the GPU busy ~0.3 s before the timed region (untimed)
+    t_end = time.perf_counter() + (0.0 if args.profile_run else 0.3)
+    while time.perf_counter() < t_end:
+        step()
+        torch.cuda.synchronize()
+    ctx.stage_times(reset=True)
+    ctx.set_profiling(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))          # evict L2 between steps (outside the step events)
+            ev[k][0].record()
+            step()
+            ev[k][1].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ctx.set_profiling(False)
+    stages = ctx.stage_times(reset=True)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    frames = world * args.steps
+    fps = frames / (tot_ms / 1e3)
+    launches = int(sum(v[1] for v in stages.values()))
+
+    # roofline of the dominant kernel (largest share of device time)
+    hbm, peak_src = peaks()
+    kern = {k: v for k, v in stages.items() if v[1] > 0}
+    dom = max(kern, key=lambda k: kern[k][0])
+    dom_ms = kern[dom][0] / kern[dom][1]
+    dom_bytes = model.get(dom, 0)
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+            "bytes_per_launch": dom_bytes, "us_per_launch": dom_ms * 1e3}
+    prof_traffic = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if os.path.exists(prof_traffic):
+        tr = json.load(open(prof_traffic)).get(dom)
+        if tr:
+            roof["traffic"] = tr
+    step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # end to end through the public API with host (pinned) buffers
+    F_h = torch.empty((1, H, W, C), pin_memory=True)
+    A_h = torch.empty((1, H, W), pin_memory=True)
+    D_h = torch.empty((1, H, W), pin_memory=True)
+    gf_h = torch.empty_like(feat_h).pin_memory()
+    go_h = torch.empty_like(op_h).pin_memory()
+    h2d = sum(t.numel() * 4 for t in (xyz_h, feat_h, op_h, gF_h, gA_h, gD_h))
+    d2h = sum(t.numel() * 4 for t in (F_h, A_h, D_h, gf_h, go_h))
+
+    def e2e_step():
+        xyz.copy_(xyz_h, non_blocking=True)
+        feat.copy_(feat_h, non_blocking=True)
+        op.copy_(op_h, non_blocking=True)
+        gF.copy_(gF_h, non_blocking=True)
+        gA.copy_(gA_h, non_blocking=True)
+        gD.copy_(gD_h, non_blocking=True)
+        step()
+        F_h.copy_(out["F"], non_blocking=True)
+        A_h.copy_(out["A"], non_blocking=True)
+        D_h.copy_(out["D"], non_blocking=True)
+        gf_h.copy_(g_feat, non_blocking=True)
+        go_h.copy_(g_op, non_blocking=True)
+
+    for _ in range(0 if args.profile_run else 2):
+        e2e_step()
+    n_e2e = 1 if args.profile_run else max(3, min(args.steps, 20))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(n_e2e):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / n_e2e
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_fps = world / (e2e_ms / 1e3)
+
+    # CPU oracle baseline (rank 0, N = 1 only): bounded sample of the same workload
+    cpu = None
+    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.profile_run):
+        th = cpu_threads()
+        gFn, gAn, gDn = (x[0] for x in synthgen.upstream_grads(2, 1, H, W, C))
+        tt, ff = 0.0, 0.0
+        while tt < 10.0:
+            t, f = oracle_step(c, gFn, gAn, gDn, 0.25, th)
+            tt += t
+            ff += f
+        cpu = {"value": ff / tt, "unit": "frames/s", "cores": th, "kind": "oracle",
+               "sample": f"{ff:.2f} frames (bands of 25 % of the 1080p rows) of cfg2 fwd+bwd, {tt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "N": N, "N_visible": Nv, "F_t": Ft, "H": H, "W": W,
+                       "C": C, "mode": "bilinear", "alpha_max": 0.99, "t_min": 1e-4,
+                       "parallelism": f"independent frames x{world} (weak)",
+                       "l2": "flushed: 256 MiB write between steps, outside the per-step events"},
+            "mpoints_per_s": fps * N / 1e6,
+            "step_algorithmic_bytes": step_bytes,
+            "step_roofline": {"achieved": step_gbs, "peak": hbm, "unit": "GB/s", "frac": step_gbs / hbm,
+                              "frac_of_nominal_8TBs": step_gbs / NOMINAL_HBM_GBS},
+            "roofline": roof,
+            "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-run", action="store_true",
+                    help="for ncu: no clock ramp, no e2e leg, no CPU baseline")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
