@@ -38,7 +38,7 @@ const char* kStageNames[kNumStages] = {"memset", "project_count", "scan_tiles", 
                                        "sort_big", "blend_fwd", "blend_bwd"};
 
 struct ViewState {
-  Buf ranges, sorted_idx, T_final, last, dbg_key, dbg_tiles, scalars;
+  Buf ranges, sorted_idx, T_final, last, dbg_key, dbg_tiles, scalars, rec;
   uint64_t idx_cap = 0;
 };
 
@@ -54,7 +54,7 @@ struct inpc_ctx {
   int num_sms = 148;
   int big_grid = 0;
   // scratch (shared by views, stream ordered)
-  Buf tile_count, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow;
+  Buf zeroed, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow;
   uint64_t entry_cap = 0;
   std::vector<ViewState> views;
   // saved-state signature
@@ -221,38 +221,60 @@ void make_dev(const inpc_raster_cfg* cfg, const inpc_camera& cam, DevCam& dc, De
 
 int cmax_for(int C) { return C <= 4 ? 4 : C <= 8 ? 8 : C <= 16 ? 16 : C <= 32 ? 32 : 64; }
 
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 template <int MODE, int CMAX>
-void launch_blend_fwd(int grid, cudaStream_t s, const DevCam& dc, const DevCfg& g, const float* xyz,
-                      const float* feat, const float* op, const float* bg, const uint32_t* ranges,
-                      const unsigned long long* entries, uint32_t* sorted_idx, const BlendOut& o) {
-  k_blend_fwd<MODE, CMAX><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, entries,
-                                                         sorted_idx, o);
+void launch_blend_fwd(int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
+                      const PointRec* rec, const float* feat, bool packed, const float* bg,
+                      const uint32_t* ranges, const unsigned long long* entries,
+                      uint32_t* sorted_idx, const BlendOut& o) {
+  const size_t smem = kWarpsPerBlock * sizeof(FwdSmem<CMAX>);
+  static bool once = (set_smem(k_blend_fwd<MODE, CMAX>, smem), true);
+  (void)once;
+  const int grid = (band_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  k_blend_fwd<MODE, CMAX><<<grid, kWarpsPerBlock * 32, smem, s>>>(dc, g, band_tiles, rec, feat, packed,
+                                                                  bg, ranges, entries, sorted_idx, o);
+}
+
+template <int MODE, int CMAX>
+void launch_blend_bwd(int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
+                      const PointRec* rec, const float* feat, bool packed, const float* bg,
+                      const uint32_t* ranges, const uint32_t* sorted_idx, const BwdIn& in) {
+  const size_t smem = kWarpsPerBlock * sizeof(BwdSmem<MODE, CMAX>);
+  static bool once = (set_smem(k_blend_bwd<MODE, CMAX>, smem), true);
+  (void)once;
+  const int grid = (band_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  k_blend_bwd<MODE, CMAX><<<grid, kWarpsPerBlock * 32, smem, s>>>(dc, g, band_tiles, rec, feat, packed,
+                                                                  bg, ranges, sorted_idx, in);
 }
 
 template <int MODE>
-void dispatch_blend_fwd(int cmax, int grid, cudaStream_t s, const DevCam& dc, const DevCfg& g,
-                        const float* xyz, const float* feat, const float* op, const float* bg,
+void dispatch_blend_fwd(int cmax, int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
+                        const PointRec* xyz, const float* feat, bool op, const float* bg,
                         const uint32_t* ranges, const unsigned long long* entries,
                         uint32_t* sorted_idx, const BlendOut& o) {
   switch (cmax) {
-    case 4: launch_blend_fwd<MODE, 4>(grid, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
-    case 8: launch_blend_fwd<MODE, 8>(grid, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
-    case 16: launch_blend_fwd<MODE, 16>(grid, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
-    case 32: launch_blend_fwd<MODE, 32>(grid, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
-    default: launch_blend_fwd<MODE, 64>(grid, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    case 4: launch_blend_fwd<MODE, 4>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    case 8: launch_blend_fwd<MODE, 8>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    case 16: launch_blend_fwd<MODE, 16>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    case 32: launch_blend_fwd<MODE, 32>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    default: launch_blend_fwd<MODE, 64>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
   }
 }
 
 template <int MODE>
-void dispatch_blend_bwd(int cmax, int grid, cudaStream_t s, const DevCam& dc, const DevCfg& g,
-                        const float* xyz, const float* feat, const float* op, const float* bg,
+void dispatch_blend_bwd(int cmax, int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
+                        const PointRec* xyz, const float* feat, bool op, const float* bg,
                         const uint32_t* ranges, const uint32_t* sorted_idx, const BwdIn& in) {
   switch (cmax) {
-    case 4: k_blend_bwd<MODE, 4><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
-    case 8: k_blend_bwd<MODE, 8><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
-    case 16: k_blend_bwd<MODE, 16><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
-    case 32: k_blend_bwd<MODE, 32><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
-    default: k_blend_bwd<MODE, 64><<<grid, kBlendThreads, 0, s>>>(dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+    case 4: launch_blend_bwd<MODE, 4>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+    case 8: launch_blend_bwd<MODE, 8>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+    case 16: launch_blend_bwd<MODE, 16>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+    case 32: launch_blend_bwd<MODE, 32>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+    default: launch_blend_bwd<MODE, 64>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
   }
 }
 
@@ -307,11 +329,12 @@ int inpc_ctx_destroy(inpc_ctx* c) {
   if (!c) return INPC_INVALID_ARG;
   DeviceGuard dg(c->device);
   cudaDeviceSynchronize();
-  for (Buf* b : {&c->tile_count, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries,
+  for (Buf* b : {&c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries,
                  &c->tmp, &c->overflow})
     free_buf(*b);
   for (auto& v : c->views)
-    for (Buf* b : {&v.ranges, &v.sorted_idx, &v.T_final, &v.last, &v.dbg_key, &v.dbg_tiles, &v.scalars})
+    for (Buf* b : {&v.ranges, &v.sorted_idx, &v.T_final, &v.last, &v.dbg_key, &v.dbg_tiles, &v.scalars,
+                   &v.rec})
       free_buf(*b);
   for (auto& e : c->pending) {
     cudaEventDestroy(e.a);
@@ -390,9 +413,13 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   const bool gauss = cfg->splat_mode == INPC_SPLAT_GAUSSIAN;
   const bool debug = (cfg->flags & INPC_FLAG_DEBUG) != 0;
   const int cmax = cmax_for(cfg->C);
+  const bool packed = !gauss && cfg->C == 4;  // features travel in the point record
 
   // scratch
-  if ((st = ensure(c->tile_count, (size_t)(T + 1) * 4, s))) return st;
+  const int scan_blocks = (T + kScanTile - 1) / kScanTile;
+  const size_t count_bytes = ((size_t)(T + 1) * 4 + 15) / 16 * 16;
+  const size_t zero_bytes = count_bytes + (size_t)scan_blocks * 8;
+  if ((st = ensure(c->zeroed, zero_bytes, s))) return st;
   if ((st = ensure(c->cursor, (size_t)(T + 1) * 4, s))) return st;
   if ((st = ensure(c->big_tiles, (size_t)(T + 1) * 4, s))) return st;
   if ((st = ensure(c->big_elem, (size_t)(T + 2) * 4, s))) return st;
@@ -410,33 +437,39 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     if ((st = ensure(vs.T_final, (size_t)P * 4, s))) return st;
     if ((st = ensure(vs.last, (size_t)P * 4, s))) return st;
     if ((st = ensure(vs.scalars, sizeof(ViewScalars), s))) return st;
+    if ((st = ensure(vs.rec, (size_t)(N > 0 ? N : 1) * sizeof(PointRec), s))) return st;
     if (debug && N > 0) {
       if ((st = ensure(vs.dbg_key, (size_t)N * 4, s))) return st;
       if ((st = ensure(vs.dbg_tiles, (size_t)N * 4, s))) return st;
     }
     const float* feat_v = feat + (size_t)v * feat_view_stride;
     const float* bg_v = bg ? bg + (size_t)v * bg_view_stride : nullptr;
-    uint32_t* tc = (uint32_t*)c->tile_count.p;
+    uint32_t* tc = (uint32_t*)c->zeroed.p;
+    unsigned long long* scan_state = (unsigned long long*)((char*)c->zeroed.p + count_bytes);
     ViewScalars* sc = (ViewScalars*)vs.scalars.p;
     {
       StageTimer tm(c, s, kStMemset, 0);
-      CK(cudaMemsetAsync(tc, 0, (size_t)(T + 1) * 4, s));
-      CK(cudaMemsetAsync(c->overflow.p, 0, 4, s));
+      CK(cudaMemsetAsync(c->zeroed.p, 0, zero_bytes, s));
+      CK(cudaMemsetAsync(sc, 0, sizeof(ViewScalars), s));
     }
-    const int nblk = (int)((N + 255) / 256);
+    const int nblk = (int)((N + (int64_t)kPointThreads * kPPT - 1) / ((int64_t)kPointThreads * kPPT));
     if (N > 0) {
       StageTimer tm(c, s, kStProject, 1);
       uint32_t* dk = debug ? (uint32_t*)vs.dbg_key.p : nullptr;
       uint32_t* dt = debug ? (uint32_t*)vs.dbg_tiles.p : nullptr;
-      if (gauss) k_project_count<1><<<nblk, 256, 0, s>>>(dc, g, xyz, N, tc, dk, dt);
-      else k_project_count<0><<<nblk, 256, 0, s>>>(dc, g, xyz, N, tc, dk, dt);
+      if (gauss)
+        k_project_count<1><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N,
+                                                           (PointRec*)vs.rec.p, tc, dk, dt);
+      else
+        k_project_count<0><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N,
+                                                           (PointRec*)vs.rec.p, tc, dk, dt);
       CK(cudaGetLastError());
     }
     {
       StageTimer tm(c, s, kStScan, 1);
-      k_scan_tiles<<<1, kScanThreads, 0, s>>>(T, tc, (uint32_t*)vs.ranges.p, (uint32_t*)c->cursor.p,
-                                             (uint32_t*)c->big_tiles.p, (uint32_t*)c->big_elem.p,
-                                             (uint32_t*)c->big_chunk.p, sc);
+      k_scan_tiles<<<scan_blocks, kScanThreads, 0, s>>>(T, tc, (uint32_t*)vs.ranges.p,
+                                                        (uint32_t*)c->cursor.p,
+                                                        (uint32_t*)c->big_tiles.p, scan_state, sc);
       CK(cudaGetLastError());
     }
     uint64_t need = bound;
@@ -454,21 +487,21 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     if (N > 0) {
       StageTimer tm(c, s, kStScatter, 1);
       if (gauss)
-        k_scatter<1><<<nblk, 256, 0, s>>>(dc, g, xyz, N, (uint32_t*)c->cursor.p,
+        k_scatter<1><<<nblk, kPointThreads, 0, s>>>(g, (const PointRec*)vs.rec.p, N, (uint32_t*)c->cursor.p,
                                           (unsigned long long*)c->entries.p, need,
                                           (uint32_t*)c->overflow.p);
       else
-        k_scatter<0><<<nblk, 256, 0, s>>>(dc, g, xyz, N, (uint32_t*)c->cursor.p,
+        k_scatter<0><<<nblk, kPointThreads, 0, s>>>(g, (const PointRec*)vs.rec.p, N, (uint32_t*)c->cursor.p,
                                           (unsigned long long*)c->entries.p, need,
                                           (uint32_t*)c->overflow.p);
       CK(cudaGetLastError());
     }
-    if (N > kSmemSortCap) {  // a tile can only exceed the SMEM cap with > cap points
+    if (N > kWarpSortCap) {  // a tile can only exceed the SMEM cap with > cap points
       StageTimer tm(c, s, kStSortBig, 1);
       const uint32_t* r = (const uint32_t*)vs.ranges.p;
       const uint32_t* bt = (const uint32_t*)c->big_tiles.p;
-      const uint32_t* be = (const uint32_t*)c->big_elem.p;
-      const uint32_t* bc = (const uint32_t*)c->big_chunk.p;
+      uint32_t* be = (uint32_t*)c->big_elem.p;
+      uint32_t* bc = (uint32_t*)c->big_chunk.p;
       const ViewScalars* scc = sc;
       unsigned long long* en = (unsigned long long*)c->entries.p;
       unsigned long long* tp = (unsigned long long*)c->tmp.p;
@@ -487,11 +520,11 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       o.T_final = (float*)vs.T_final.p;
       o.last = (uint32_t*)vs.last.p;
       if (gauss)
-        dispatch_blend_fwd<1>(cmax, band_tiles, s, dc, g, xyz, feat_v, opacity, bg_v,
+        dispatch_blend_fwd<1>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, false, bg_v,
                               (const uint32_t*)vs.ranges.p, (const unsigned long long*)c->entries.p,
                               (uint32_t*)vs.sorted_idx.p, o);
       else
-        dispatch_blend_fwd<0>(cmax, band_tiles, s, dc, g, xyz, feat_v, opacity, bg_v,
+        dispatch_blend_fwd<0>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, packed, bg_v,
                               (const uint32_t*)vs.ranges.p, (const unsigned long long*)c->entries.p,
                               (uint32_t*)vs.sorted_idx.p, o);
       CK(cudaGetLastError());
@@ -551,6 +584,7 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   const int band_tiles = (g.ty1 - g.ty0) * g.tiles_x;
   const bool gauss = cfg->splat_mode == INPC_SPLAT_GAUSSIAN;
   const int cmax = cmax_for(cfg->C);
+  const bool packed = !gauss && cfg->C == 4;
   for (int v = 0; v < V; ++v) {
     make_dev(cfg, cams[v], dc, g);
     ViewState& vs = c->views[v];
@@ -566,10 +600,10 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     const float* bg_v = bg ? bg + (size_t)v * bg_view_stride : nullptr;
     StageTimer tm(c, s, kStBlendBwd, 1);
     if (gauss)
-      dispatch_blend_bwd<1>(cmax, band_tiles, s, dc, g, xyz, feat_v, opacity, bg_v,
+      dispatch_blend_bwd<1>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, false, bg_v,
                             (const uint32_t*)vs.ranges.p, (const uint32_t*)vs.sorted_idx.p, in);
     else
-      dispatch_blend_bwd<0>(cmax, band_tiles, s, dc, g, xyz, feat_v, opacity, bg_v,
+      dispatch_blend_bwd<0>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, packed, bg_v,
                             (const uint32_t*)vs.ranges.p, (const uint32_t*)vs.sorted_idx.p, in);
     CK(cudaGetLastError());
   }

@@ -1,21 +1,23 @@
 // kernels.cuh — the sm_100a kernels of the rasterizer hot path (H1-H8).
 //
 //   k_project_count  H1+H2: project, footprint, count entries per 8x8 tile
-//   k_scan_tiles     H3:    exclusive scan of tile counts -> tile ranges, F_t;
-//                           list of tiles too large for the in-SMEM sort
+//   k_scan_tiles     H3:    decoupled look-back exclusive scan of the tile
+//                           counts -> tile ranges, F_t; list of big tiles
 //   k_scatter        H5:    write (depth key << 32 | point index) into the
 //                           tile buckets (bucket order arbitrary)
-//   k_sort_big       H4+H6 for tiles over the SMEM cap: chunk sort + merge
-//                           passes (cooperative, grid-synchronised)
-//   k_blend_fwd      H4+H6 for the other tiles (bitonic sort of the unique
-//                           64-bit keys in SMEM) fused with H7: front-to-back
-//                           blend, Eq. 1, alpha clamp, early termination
-//   k_blend_bwd      H8:    reverse-order backward, Eq. 2 corrected
+//   k_sort_big       H4+H6 for tiles over the warp-sort cap: SMEM chunk
+//                           sort + merge passes (cooperative, grid sync)
+//   k_blend_fwd      H4+H6 for the other tiles (warp bitonic sort of the
+//                           unique 64-bit keys) fused with H7: one warp per
+//                           8x8 tile, per-pixel fragment bitmasks, front-to-
+//                           back blend (Eq. 1), alpha clamp, early termination
+//   k_blend_bwd      H8:    one warp per tile, reverse-order backward
+//                           (Eq. 2 corrected), SMEM pre-reduction per point
 //
 // The two-stage sort of the paper (depth sort of the points, then
 // a stable sort of the tile copies by tile key) is replaced by a bucket
-// scatter + per-tile sort of the unique (depth, index) key: same per-tile
-// lists bit for bit, a fraction of the sort traffic.
+// scatter + per-tile sort of the unique (depth, index) key: the same per-tile
+// lists bit for bit at a fraction of the sort traffic.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -23,46 +25,125 @@
 
 namespace inpc {
 
-constexpr int kBlendThreads = 64;    // one thread per pixel of an 8x8 tile
-constexpr int kSmemSortCap = 1024;   // tiles above this go through k_sort_big
+constexpr int kWarpsPerBlock = 4;    // blend kernels: one warp per tile
+constexpr int kWarpSortCap = 256;    // tiles above this go through k_sort_big
 constexpr int kBigChunk = 2048;      // chunk of k_sort_big's SMEM sort
 constexpr int kBigThreads = 512;
-constexpr int kScanThreads = 1024;
-constexpr int kScanItems = 8;
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;        // tiles per scan thread
+constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int kPointThreads = 256;
+constexpr int kPPT = 4;              // points per thread in the point kernels
 
 // ---------------------------------------------------------------- H1 + H2
+// Per-point record written once by the projection kernel and gathered by
+// every later stage (one 32-byte sector per point instead of xyz + o + f
+// scattered over three arrays):
+//   bilinear: u, v, z_c, o, f0..f3 (features packed when C == 4, else 0)
+//   Gaussian: u, v, z_c, o, conic a, b, c, radius r
+// z_c = 0 marks a point without footprint (culled or off image).
+struct __align__(16) PointRec {
+  float4 a;  // u, v, z_c, o
+  float4 b;  // features | conic + radius
+};
+
+// kPPT points per thread, loads of all of them issued before any compute so
+// enough bytes are in flight to cover HBM latency.
 template <int MODE>
-__global__ void __launch_bounds__(256) k_project_count(DevCam cam, DevCfg g, const float* __restrict__ xyz,
-                                                       int64_t N, uint32_t* __restrict__ tile_count,
-                                                       uint32_t* __restrict__ dbg_key,
-                                                       uint32_t* __restrict__ dbg_tiles) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  Proj p;
-  Foot f;
-  bool vis = false, ok = false;
-  {
-    float X = __ldg(xyz + 3 * i), Y = __ldg(xyz + 3 * i + 1), Z = __ldg(xyz + 3 * i + 2);
-    vis = project_point(cam, X, Y, Z, p);
-    if (vis) ok = MODE == 0 ? foot_bilinear(g, p, f) : foot_gauss(cam, g, p, f);
+__global__ void __launch_bounds__(kPointThreads) k_project_count(
+    DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ opacity,
+    const float* __restrict__ feat, bool pack, int64_t N, PointRec* __restrict__ rec,
+    uint32_t* __restrict__ tile_count, uint32_t* __restrict__ dbg_key,
+    uint32_t* __restrict__ dbg_tiles) {
+  const int64_t stride = (int64_t)gridDim.x * kPointThreads;
+  const int64_t i0 = (int64_t)blockIdx.x * kPointThreads + threadIdx.x;
+  float X[kPPT], Y[kPPT], Z[kPPT], O[kPPT];
+  float4 Fv[kPPT];
+#pragma unroll
+  for (int k = 0; k < kPPT; ++k) {
+    int64_t i = i0 + k * stride;
+    if (i < N) {
+      X[k] = __ldg(xyz + 3 * i);
+      Y[k] = __ldg(xyz + 3 * i + 1);
+      Z[k] = __ldg(xyz + 3 * i + 2);
+      O[k] = __ldg(opacity + i);
+      if (MODE == 0 && pack) Fv[k] = __ldg(reinterpret_cast<const float4*>(feat) + i);
+    }
   }
-  if (dbg_key) {
-    dbg_key[i] = vis ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
-    dbg_tiles[i] = ok ? (uint32_t)((f.xhi / kTile - f.xlo / kTile + 1) * (f.yhi / kTile - f.ylo / kTile + 1))
-                      : 0u;
+#pragma unroll
+  for (int k = 0; k < kPPT; ++k) {
+    int64_t i = i0 + k * stride;
+    if (i >= N) break;
+    Proj p;
+    Foot f;
+    float ca = 0.f, cb = 0.f, cc = 0.f, r = 0.f;
+    bool vis = project_point(cam, X[k], Y[k], Z[k], p);
+    bool ok = false;
+    if (vis) {
+      if (MODE == 0) ok = foot_bilinear(g, p.u, p.v, f);
+      else ok = gauss_conic(cam, g, p, ca, cb, cc, r) && gauss_rect(g, p.u, p.v, r, f);
+    }
+    PointRec pr;
+    pr.a = make_float4(p.u, p.v, ok ? p.zc : 0.0f, O[k]);
+    if (MODE == 0) pr.b = pack ? Fv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    else pr.b = make_float4(ca, cb, cc, r);
+    rec[i] = pr;
+    if (dbg_key) {
+      dbg_key[i] = vis ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
+      dbg_tiles[i] = ok ? (uint32_t)((f.xhi / kTile - f.xlo / kTile + 1) *
+                                     (f.yhi / kTile - f.ylo / kTile + 1))
+                        : 0u;
+    }
+    if (!ok) continue;
+    int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
+    int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
+    for (int ty = ty_lo; ty <= ty_hi; ++ty)
+      for (int tx = tx_lo; tx <= tx_hi; ++tx) atomicAdd(tile_count + (size_t)ty * g.tiles_x + tx, 1u);
   }
-  if (!ok) return;
-  int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
-  int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
-  for (int ty = ty_lo; ty <= ty_hi; ++ty)
-    for (int tx = tx_lo; tx <= tx_hi; ++tx) atomicAdd(tile_count + (size_t)ty * g.tiles_x + tx, 1u);
+}
+
+// Footprint rectangle of a point from its record (same ops as at projection).
+template <int MODE>
+__device__ __forceinline__ bool rec_foot(const DevCfg& g, float4 a, float radius, Foot& f) {
+  if (!(a.z > 0.0f)) return false;
+  if (MODE == 0) return foot_bilinear(g, a.x, a.y, f);
+  return gauss_rect(g, a.x, a.y, radius, f);
 }
 
 // ---------------------------------------------------------------- H3
-// Block-wide exclusive scan of one value per thread (kScanThreads threads).
-__device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* warp_tot, uint32_t& total) {
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t x = v;
+// Scalars shared between the kernels of one view (device memory, zeroed
+// before k_scan_tiles).
+struct ViewScalars {
+  uint32_t Ft;       // total tile entries
+  uint32_t num_big;  // tiles with more than kWarpSortCap entries
+  uint32_t max_big;  // largest of them
+  uint32_t ticket;   // scan CTA ticket
+};
+
+// Decoupled look-back scan (one pass over the counts): each CTA scans
+// kScanTile counts, publishes its aggregate, and adds the prefix found by
+// walking back over its predecessors' published values.
+// state[b] = flag << 32 | value, flag 1 = aggregate, 2 = inclusive prefix.
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
+    int T, const uint32_t* __restrict__ count, uint32_t* __restrict__ ranges,
+    uint32_t* __restrict__ cursor, uint32_t* __restrict__ big_tiles,
+    unsigned long long* state, ViewScalars* sc) {
+  __shared__ uint32_t warp_tot[kScanThreads / 32];
+  __shared__ uint32_t s_prefix, s_bid;
+  if (threadIdx.x == 0) s_bid = atomicAdd(&sc->ticket, 1u);
+  __syncthreads();
+  const uint32_t bid = s_bid;
+  const int i0 = bid * kScanTile + threadIdx.x * kScanItems;
+  uint32_t c[kScanItems];
+  uint32_t sum = 0, mx = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    c[k] = (i0 + k < T) ? count[i0 + k] : 0u;
+    sum += c[k];
+  }
+  // block exclusive scan of the per-thread sums
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -71,118 +152,100 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* warp_tot,
   if (lane == 31) warp_tot[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    uint32_t w = lane < (kScanThreads / 32) ? warp_tot[lane] : 0u;
+    uint32_t w = lane < kScanThreads / 32 ? warp_tot[lane] : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += y;
     }
-    warp_tot[lane] = w;  // inclusive warp prefix
+    if (lane < kScanThreads / 32) warp_tot[lane] = w;
   }
   __syncthreads();
-  uint32_t base = wid ? warp_tot[wid - 1] : 0u;
-  total = warp_tot[kScanThreads / 32 - 1];
-  __syncthreads();
-  return base + x - v;
-}
-
-// Scalars shared between kernels of one view (device memory).
-struct ViewScalars {
-  uint32_t Ft;        // total tile entries
-  uint32_t num_big;   // tiles with more than kSmemSortCap entries
-  uint32_t max_big;   // largest of them
-  uint32_t pad;
-};
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
-    int T, const uint32_t* __restrict__ count, uint32_t* __restrict__ ranges,
-    uint32_t* __restrict__ cursor, uint32_t* __restrict__ big_tiles, uint32_t* __restrict__ big_elem,
-    uint32_t* __restrict__ big_chunk, ViewScalars* sc) {
-  __shared__ uint32_t wt[32];
-  uint32_t carry = 0, carry_big = 0, carry_be = 0, carry_bc = 0, maxbig = 0;
-  for (int base = 0; base < T; base += kScanThreads * kScanItems) {
-    int i0 = base + threadIdx.x * kScanItems;
-    uint32_t c[kScanItems];
-    uint32_t s = 0, nb = 0, be = 0, bc = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-      c[k] = (i0 + k < T) ? count[i0 + k] : 0u;
-      s += c[k];
-      if (c[k] > (uint32_t)kSmemSortCap) {
-        nb++;
-        be += c[k];
-        bc += (c[k] + kBigChunk - 1) / kBigChunk;
-        maxbig = max(maxbig, c[k]);
-      }
-    }
-    uint32_t tot, tot_nb, tot_be, tot_bc;
-    uint32_t off = block_exscan(s, wt, tot) + carry;
-    uint32_t off_nb = block_exscan(nb, wt, tot_nb) + carry_big;
-    uint32_t off_be = block_exscan(be, wt, tot_be) + carry_be;
-    uint32_t off_bc = block_exscan(bc, wt, tot_bc) + carry_bc;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-      if (i0 + k < T) {
-        ranges[i0 + k] = off;
-        cursor[i0 + k] = off;
-        if (c[k] > (uint32_t)kSmemSortCap) {
-          big_tiles[off_nb] = i0 + k;
-          big_elem[off_nb] = off_be;
-          big_chunk[off_nb] = off_bc;
-          off_nb++;
-          off_be += c[k];
-          off_bc += (c[k] + kBigChunk - 1) / kBigChunk;
-        }
-      }
-      off += c[k];
-    }
-    carry += tot;
-    carry_big += tot_nb;
-    carry_be += tot_be;
-    carry_bc += tot_bc;
-  }
-  // max over threads
-  for (int o = 16; o > 0; o >>= 1) maxbig = max(maxbig, __shfl_xor_sync(0xffffffffu, maxbig, o));
-  __shared__ uint32_t smax;
-  if (threadIdx.x == 0) smax = 0;
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) atomicMax(&smax, maxbig);
-  __syncthreads();
+  const uint32_t excl = (wid ? warp_tot[wid - 1] : 0u) + x - sum;
+  const uint32_t agg = warp_tot[kScanThreads / 32 - 1];
   if (threadIdx.x == 0) {
-    ranges[T] = carry;
-    big_elem[carry_big] = carry_be;
-    big_chunk[carry_big] = carry_bc;
-    sc->Ft = carry;
-    sc->num_big = carry_big;
-    sc->max_big = smax;
+    volatile unsigned long long* vs = state;
+    if (bid == 0) {
+      vs[0] = (2ull << 32) | agg;
+      s_prefix = 0;
+    } else {
+      vs[bid] = (1ull << 32) | agg;
+      uint32_t prefix = 0;
+      int b = (int)bid - 1;
+      while (true) {
+        unsigned long long v = vs[b];
+        uint32_t flag = (uint32_t)(v >> 32);
+        if (flag == 0) continue;  // predecessor not published yet
+        prefix += (uint32_t)v;
+        if (flag == 2) break;
+        --b;
+      }
+      __threadfence();
+      vs[bid] = (2ull << 32) | (prefix + agg);
+      s_prefix = prefix;
+    }
+  }
+  __syncthreads();
+  uint32_t off = s_prefix + excl;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (i0 + k < T) {
+      ranges[i0 + k] = off;
+      cursor[i0 + k] = off;
+      if (c[k] > (uint32_t)kWarpSortCap) {
+        big_tiles[atomicAdd(&sc->num_big, 1u)] = i0 + k;
+        mx = max(mx, c[k]);
+      }
+    }
+    off += c[k];
+  }
+  if (mx) atomicMax(&sc->max_big, mx);
+  if (i0 < T && i0 + kScanItems >= T) {  // the thread owning the last tile
+    ranges[T] = off;
+    sc->Ft = off;
   }
 }
 
 // ---------------------------------------------------------------- H5
 template <int MODE>
-__global__ void __launch_bounds__(256) k_scatter(DevCam cam, DevCfg g, const float* __restrict__ xyz,
-                                                 int64_t N, uint32_t* __restrict__ cursor,
-                                                 unsigned long long* __restrict__ entries,
-                                                 uint64_t cap, uint32_t* __restrict__ overflow) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  Proj p;
-  Foot f;
-  if (!point_foot<MODE>(cam, g, xyz, i, p, f)) return;
-  unsigned long long kv = ((unsigned long long)__float_as_uint(p.zc) << 32) | (uint32_t)i;
-  int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
-  int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
-  for (int ty = ty_lo; ty <= ty_hi; ++ty)
-    for (int tx = tx_lo; tx <= tx_hi; ++tx) {
-      uint32_t pos = atomicAdd(cursor + (size_t)ty * g.tiles_x + tx, 1u);
-      if (pos < cap) entries[pos] = kv;
-      else atomicOr(overflow, 1u);
+__global__ void __launch_bounds__(kPointThreads) k_scatter(
+    DevCfg g, const PointRec* __restrict__ rec, int64_t N, uint32_t* __restrict__ cursor,
+    unsigned long long* __restrict__ entries, uint64_t cap, uint32_t* __restrict__ overflow) {
+  const int64_t stride = (int64_t)gridDim.x * kPointThreads;
+  const int64_t i0 = (int64_t)blockIdx.x * kPointThreads + threadIdx.x;
+  float4 A[kPPT];
+  float Rd[kPPT];
+#pragma unroll
+  for (int k = 0; k < kPPT; ++k) {
+    int64_t i = i0 + k * stride;
+    Rd[k] = 0.0f;
+    if (i < N) {
+      A[k] = __ldg(&rec[i].a);
+      if (MODE == 1) Rd[k] = __ldg(&rec[i].b.w);
     }
+  }
+#pragma unroll
+  for (int k = 0; k < kPPT; ++k) {
+    int64_t i = i0 + k * stride;
+    if (i >= N) break;
+    Foot f;
+    if (!rec_foot<MODE>(g, A[k], Rd[k], f)) continue;
+    unsigned long long kv = ((unsigned long long)__float_as_uint(A[k].z) << 32) | (uint32_t)i;
+    int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
+    int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
+    for (int ty = ty_lo; ty <= ty_hi; ++ty)
+      for (int tx = tx_lo; tx <= tx_hi; ++tx) {
+        uint32_t pos = atomicAdd(cursor + (size_t)ty * g.tiles_x + tx, 1u);
+        if (pos < cap) entries[pos] = kv;
+        else atomicOr(overflow, 1u);
+      }
+  }
 }
 
 // ---------------------------------------------------------------- sort helpers
-// In-place ascending bitonic sort of np (power of two) 64-bit keys in SMEM.
-__device__ __forceinline__ void smem_bitonic(unsigned long long* s, int np) {
+// In-place ascending bitonic sort of np (power of two) 64-bit keys in SMEM by
+// the whole block.
+__device__ __forceinline__ void block_bitonic(unsigned long long* s, int np) {
   for (int k = 2; k <= np; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int t = threadIdx.x; t < (np >> 1); t += blockDim.x) {
@@ -196,6 +259,48 @@ __device__ __forceinline__ void smem_bitonic(unsigned long long* s, int np) {
         }
       }
       __syncthreads();
+    }
+}
+
+// Warp-level sort of n <= kWarpSortCap unique 64-bit keys read from src into
+// keys[0..n) (SMEM).  n <= 32: register bitonic over shuffles; otherwise a
+// warp-synchronous SMEM bitonic network.
+__device__ __forceinline__ void warp_sort(unsigned long long* keys,
+                                          const unsigned long long* __restrict__ src, int n,
+                                          int lane) {
+  if (n <= 32) {
+    unsigned long long v = lane < n ? src[lane] : ~0ull;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        unsigned long long o = __shfl_xor_sync(0xffffffffu, v, j);
+        bool up = (lane & k) == 0;
+        bool lower = (lane & j) == 0;
+        // lower element keeps min when ascending
+        v = (lower == up) ? (o < v ? o : v) : (o > v ? o : v);
+      }
+    keys[lane] = v;
+    __syncwarp();
+    return;
+  }
+  int np = 64;
+  while (np < n) np <<= 1;
+  for (int k = lane; k < np; k += 32) keys[k] = k < n ? src[k] : ~0ull;
+  __syncwarp();
+  for (int k = 2; k <= np; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = lane; t < (np >> 1); t += 32) {
+        int i = 2 * t - (t & (j - 1));
+        int ixj = i + j;
+        unsigned long long a = keys[i], b = keys[ixj];
+        bool up = (i & k) == 0;
+        if ((a > b) == up) {
+          keys[i] = b;
+          keys[ixj] = a;
+        }
+      }
+      __syncwarp();
     }
 }
 
@@ -220,19 +325,58 @@ __device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a,
   return lo;
 }
 
-// H4+H6 for big tiles: (1) sort chunks of kBigChunk keys in SMEM, (2) merge
-// runs pairwise (rank by binary search; keys are unique), grid-synchronised,
-// (3) write the point indices to sorted_idx.  Exits at once if no tile is big.
+// H4+H6 for big tiles (more than kWarpSortCap entries): (0) block 0 builds
+// the element / chunk prefixes of the big-tile list, (1) chunks of kBigChunk
+// keys are sorted in SMEM, (2) runs are merged pairwise (rank by binary
+// search; keys are unique), (3) the point indices go to sorted_idx.  Grid-
+// synchronised between phases; returns at once if no tile is big.
 __global__ void __launch_bounds__(kBigThreads) k_sort_big(
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles,
-    const uint32_t* __restrict__ big_elem, const uint32_t* __restrict__ big_chunk,
-    const ViewScalars* sc, unsigned long long* entries, unsigned long long* tmp,
-    uint32_t* __restrict__ sorted_idx) {
+    uint32_t* big_elem, uint32_t* big_chunk, const ViewScalars* sc,
+    unsigned long long* entries, unsigned long long* tmp, uint32_t* __restrict__ sorted_idx) {
   namespace cg = cooperative_groups;
   const uint32_t nb = sc->num_big;
   if (nb == 0) return;
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long s[kBigChunk];
+  __shared__ uint32_t carry[2];
+  if (blockIdx.x == 0) {
+    // exclusive prefixes of sizes and chunk counts (list order is arbitrary;
+    // it only decides which CTA works on what)
+    uint32_t* tot = reinterpret_cast<uint32_t*>(s);
+    if (threadIdx.x == 0) carry[0] = carry[1] = 0;
+    __syncthreads();
+    for (uint32_t b0 = 0; b0 < nb; b0 += blockDim.x) {
+      uint32_t j = b0 + threadIdx.x;
+      uint32_t sz = 0, ch = 0;
+      if (j < nb) {
+        uint32_t t = big_tiles[j];
+        sz = ranges[t + 1] - ranges[t];
+        ch = (sz + kBigChunk - 1) / kBigChunk;
+      }
+      tot[threadIdx.x] = sz;
+      tot[kBigThreads + threadIdx.x] = ch;
+      __syncthreads();
+      if (threadIdx.x == 0) {  // serial per 512 tiles: big tiles are few
+        uint32_t a = carry[0], c = carry[1];
+        for (uint32_t k = 0; k < blockDim.x && b0 + k < nb; ++k) {
+          big_elem[b0 + k] = a;
+          big_chunk[b0 + k] = c;
+          a += tot[k];
+          c += tot[kBigThreads + k];
+        }
+        carry[0] = a;
+        carry[1] = c;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      big_elem[nb] = carry[0];
+      big_chunk[nb] = carry[1];
+    }
+    __syncthreads();
+  }
+  grid.sync();
   const uint32_t total_chunks = big_chunk[nb], total = big_elem[nb], maxn = sc->max_big;
   for (uint32_t gch = blockIdx.x; gch < total_chunks; gch += gridDim.x) {
     uint32_t j = upper_bound_u32(big_chunk, nb, gch) - 1;
@@ -242,7 +386,7 @@ __global__ void __launch_bounds__(kBigThreads) k_sort_big(
     uint32_t n = min((uint32_t)kBigChunk, ranges[t + 1] - begin);
     for (int k = threadIdx.x; k < kBigChunk; k += blockDim.x) s[k] = k < (int)n ? entries[begin + k] : ~0ull;
     __syncthreads();
-    smem_bitonic(s, kBigChunk);
+    block_bitonic(s, kBigChunk);
     for (int k = threadIdx.x; k < (int)n; k += blockDim.x) entries[begin + k] = s[k];
     __syncthreads();
   }
@@ -279,76 +423,100 @@ __global__ void __launch_bounds__(kBigThreads) k_sort_big(
   }
 }
 
-// ---------------------------------------------------------------- H7 / H8 shared staging
-// One chunk (kBlendThreads entries) of a tile list staged in SMEM, SoA.
+// ---------------------------------------------------------------- H7 / H8 per-warp staging
+// One chunk of 32 tile-list entries staged in SMEM (SoA, slot = lane) plus
+// the per-pixel fragment masks of the chunk: bit e of mask[p] is set when
+// entry e has a (possible) fragment at tile pixel p = 8*row + col.
+//   bilinear: block origin (x0, y0) and, per block corner k = 2 dy + dx,
+//             the weight w_k (pinned fp32, R1/R3)
+//   Gaussian: u, v and the conic; the pixel lane evaluates q and w (R17)
 template <int CMAX>
 struct ChunkSmem {
-  int xlo[kBlendThreads], xhi[kBlendThreads], ylo[kBlendThreads], yhi[kBlendThreads];
-  float pa[kBlendThreads], pb[kBlendThreads];   // bilinear fa, fb | Gaussian u, v
-  float ca[kBlendThreads], cb[kBlendThreads], cc[kBlendThreads];
-  float o[kBlendThreads], z[kBlendThreads];
-  float f[kBlendThreads][CMAX];
+  int x0[32], y0[32];
+  float wc[32][4];              // bilinear corner weights
+  float u[32], v[32], ca[32], cb[32], cc[32];  // Gaussian
+  float o[32], z[32];
+  float f[32][CMAX];
+  uint32_t mask[64];
+  uint32_t idx[32];
 };
 
+template <int CMAX>
+struct FwdSmem {
+  unsigned long long keys[kWarpSortCap];
+  ChunkSmem<CMAX> ch;
+};
+
+// Backward per-warp SMEM.  Bilinear with CMAX <= 8: every fragment of an
+// entry in the tile is one of its 2x2 block corners, so each fragment owns a
+// slot [entry][corner] and the per-point sums need no SMEM atomics (float
+// atomicAdd on SMEM is a CAS loop on this part).  Otherwise SMEM atomics.
 template <int MODE, int CMAX>
-__device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int slot, const DevCam& cam,
-                                            const DevCfg& g, const float* __restrict__ xyz,
-                                            const float* __restrict__ feat,
-                                            const float* __restrict__ opacity, uint32_t idx) {
-  Proj p;
+struct BwdSmem {
+  static constexpr bool kSlots = MODE == 0 && CMAX <= 8;
+  static constexpr int kStride = kSlots ? 4 * (CMAX + 1) + 1 : CMAX + 2;  // odd: no bank conflicts
+  ChunkSmem<CMAX> ch;
+  float acc[32][kStride];
+  int touched[32];
+};
+
+// Stage tile-list entry `idx` in slot `lane` and mark its pixels of the tile
+// (origin tx0, ty0) in the chunk masks.
+template <int MODE, int CMAX>
+__device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const DevCfg& g,
+                                            const PointRec* __restrict__ rec,
+                                            const float* __restrict__ feat, bool packed,
+                                            uint32_t idx, int tx0, int ty0) {
+  const float4 A = __ldg(&rec[idx].a);
+  const float4 B = __ldg(&rec[idx].b);
   Foot f;
-  bool ok = point_foot<MODE>(cam, g, xyz, idx, p, f);
-  // a listed point always has a footprint; guard anyway (empty rectangle)
-  if (!ok) {
-    f.xlo = 1;
-    f.xhi = 0;
-    f.ylo = 1;
-    f.yhi = 0;
-  }
-  cs.xlo[slot] = f.xlo;
-  cs.xhi[slot] = f.xhi;
-  cs.ylo[slot] = f.ylo;
-  cs.yhi[slot] = f.yhi;
+  bool ok = rec_foot<MODE>(g, A, B.w, f);
+  cs.idx[lane] = idx;
+  cs.o[lane] = A.w;
+  cs.z[lane] = A.z;
   if (MODE == 0) {
-    cs.pa[slot] = f.fa;
-    cs.pb[slot] = f.fb;
-    cs.ca[slot] = __int_as_float(f.x0);
-    cs.cb[slot] = __int_as_float(f.y0);
+    cs.x0[lane] = f.x0;
+    cs.y0[lane] = f.y0;
+    const float fa1 = __fsub_rn(1.0f, f.fa), fb1 = __fsub_rn(1.0f, f.fb);
+    *reinterpret_cast<float4*>(&cs.wc[lane][0]) =
+        make_float4(__fmul_rn(fa1, fb1), __fmul_rn(f.fa, fb1), __fmul_rn(fa1, f.fb),
+                    __fmul_rn(f.fa, f.fb));
   } else {
-    cs.pa[slot] = p.u;
-    cs.pb[slot] = p.v;
-    cs.ca[slot] = f.ca;
-    cs.cb[slot] = f.cb;
-    cs.cc[slot] = f.cc;
+    cs.u[lane] = A.x;
+    cs.v[lane] = A.y;
+    cs.ca[lane] = B.x;
+    cs.cb[lane] = B.y;
+    cs.cc[lane] = B.z;
   }
-  cs.o[slot] = __ldg(opacity + idx);
-  cs.z[slot] = p.zc;
-  if (CMAX == 4 && g.C == 4) {
-    float4 v = __ldg(reinterpret_cast<const float4*>(feat) + idx);
-    cs.f[slot][0] = v.x;
-    cs.f[slot][1] = v.y;
-    cs.f[slot][2] = v.z;
-    cs.f[slot][3] = v.w;
+  if (CMAX == 4 && packed) {
+    *reinterpret_cast<float4*>(&cs.f[lane][0]) = B;
+  } else if (CMAX == 4 && g.C == 4) {
+    *reinterpret_cast<float4*>(&cs.f[lane][0]) = __ldg(reinterpret_cast<const float4*>(feat) + idx);
   } else {
 #pragma unroll
     for (int c = 0; c < CMAX; ++c)
-      if (c < g.C) cs.f[slot][c] = __ldg(feat + (size_t)idx * g.C + c);
+      if (c < g.C) cs.f[lane][c] = __ldg(feat + (size_t)idx * g.C + c);
   }
+  if (!ok) return;
+  // footprint rectangle clipped to the tile, tile-local coordinates
+  const int xl = max(f.xlo, tx0) - tx0, xh = min(f.xhi, tx0 + kTile - 1) - tx0;
+  const int yl = max(f.ylo, ty0) - ty0, yh = min(f.yhi, ty0 + kTile - 1) - ty0;
+  for (int yy = yl; yy <= yh; ++yy)
+    for (int xx = xl; xx <= xh; ++xx) atomicOr(&cs.mask[yy * kTile + xx], 1u << lane);
 }
 
-// Weight of the staged entry e at pixel (px, py); false if not a fragment.
+// Fragment weight of staged entry e at pixel (px, py) and its block corner.
+// Bilinear: every pixel of the rectangle is a fragment.  Gaussian: q <= 9.
 template <int MODE, int CMAX>
 __device__ __forceinline__ bool entry_weight(const ChunkSmem<CMAX>& cs, int e, int px, int py,
-                                             float& w) {
-  if (px < cs.xlo[e] || px > cs.xhi[e] || py < cs.ylo[e] || py > cs.yhi[e]) return false;
+                                             float& w, int& corner) {
   if (MODE == 0) {
-    int dx = px - __float_as_int(cs.ca[e]), dy = py - __float_as_int(cs.cb[e]);
-    float wx = dx ? cs.pa[e] : __fsub_rn(1.0f, cs.pa[e]);
-    float wy = dy ? cs.pb[e] : __fsub_rn(1.0f, cs.pb[e]);
-    w = __fmul_rn(wx, wy);
+    corner = 2 * (py - cs.y0[e]) + (px - cs.x0[e]);
+    w = cs.wc[e][corner];
     return true;
   } else {
-    float q = gauss_q(cs.ca[e], cs.cb[e], cs.cc[e], cs.pa[e], cs.pb[e], px, py);
+    corner = 0;
+    float q = gauss_q(cs.ca[e], cs.cb[e], cs.cc[e], cs.u[e], cs.v[e], px, py);
     if (!(q <= 9.0f)) return false;
     w = expf(__fmul_rn(-0.5f, q));
     return true;
@@ -356,220 +524,321 @@ __device__ __forceinline__ bool entry_weight(const ChunkSmem<CMAX>& cs, int e, i
 }
 
 struct BlendOut {
-  float* F;          // [H,W,C]
-  float* A;          // [H,W] or null
-  float* D;          // [H,W] or null
-  int32_t* nfrag;    // or null
-  int32_t* ncontrib; // or null
-  float* T_final;    // saved [H,W]
-  uint32_t* last;    // saved [H,W]: list position + 1 of the last composited fragment
+  float* F;           // [H,W,C]
+  float* A;           // [H,W] or null
+  float* D;           // [H,W] or null
+  int32_t* nfrag;     // or null
+  int32_t* ncontrib;  // or null
+  float* T_final;     // saved [H,W]
+  uint32_t* last;     // saved [H,W]: list position + 1 of the last composited fragment
 };
 
-// ---------------------------------------------------------------- H4/H6 (small tiles) + H7
+template <int CMAX>
+struct PixFwd {
+  float T, D;
+  float F[CMAX];
+  uint32_t last;
+  int nfrag, ncontrib;
+  bool done;
+};
+
+// Composite the fragments of one pixel in this chunk (bits of m, ascending =
+// list order), Eq. 1 with alpha clamp (R5) and early termination (R6).
 template <int MODE, int CMAX>
-__global__ void __launch_bounds__(kBlendThreads) k_blend_fwd(
-    DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ feat,
-    const float* __restrict__ opacity, const float* __restrict__ bg,
-    const uint32_t* __restrict__ ranges, const unsigned long long* __restrict__ entries,
-    uint32_t* __restrict__ sorted_idx, BlendOut out) {
-  __shared__ unsigned long long skey[kSmemSortCap];
-  __shared__ ChunkSmem<CMAX> cs;
-  const int tile = g.ty0 * g.tiles_x + blockIdx.x;
-  const int tx = tile % g.tiles_x, ty = tile / g.tiles_x;
-  const int px = tx * kTile + (threadIdx.x & 7), py = ty * kTile + (threadIdx.x >> 3);
-  const bool inside = px < g.W && py < g.H;
-  const uint32_t begin = ranges[tile], n = ranges[tile + 1] - begin;
-  const bool small = n <= (uint32_t)kSmemSortCap;
-  if (small && n > 0) {
-    int np = 64;
-    while (np < (int)n) np <<= 1;
-    for (int k = threadIdx.x; k < np; k += kBlendThreads) skey[k] = k < (int)n ? entries[begin + k] : ~0ull;
-    __syncthreads();
-    smem_bitonic(skey, np);
-    for (int k = threadIdx.x; k < (int)n; k += kBlendThreads) sorted_idx[begin + k] = (uint32_t)skey[k];
-  }
-  const bool count_frags = out.nfrag != nullptr;
-  float T = 1.0f, Dv = 0.0f;
-  float Fv[CMAX];
-#pragma unroll
-  for (int c = 0; c < CMAX; ++c) Fv[c] = 0.0f;
-  uint32_t last = 0;
-  int nfrag = 0, ncontrib = 0;
-  bool done = !inside;
-  for (uint32_t base = 0; base < n; base += kBlendThreads) {
-    uint32_t j = base + threadIdx.x;
-    __syncthreads();  // previous chunk fully consumed
-    if (j < n) {
-      uint32_t idx = small ? (uint32_t)skey[j] : sorted_idx[begin + j];
-      stage_entry<MODE, CMAX>(cs, threadIdx.x, cam, g, xyz, feat, opacity, idx);
+__device__ __forceinline__ void blend_pixel(const ChunkSmem<CMAX>& cs, const DevCfg& g,
+                                            uint32_t m, int px, int py, uint32_t base,
+                                            bool count, PixFwd<CMAX>& s) {
+  if (s.done && !count) return;
+  while (m) {
+    const int e = __ffs(m) - 1;
+    m &= m - 1;
+    float w;
+    int corner;
+    if (!entry_weight<MODE, CMAX>(cs, e, px, py, w, corner)) continue;
+    s.nfrag++;
+    if (s.done) continue;
+    const float alpha = fminf(__fmul_rn(cs.o[e], w), g.amax);
+    const float Tn = __fmul_rn(s.T, __fsub_rn(1.0f, alpha));
+    if (Tn < g.tmin) {
+      s.done = true;
+      if (!count) return;
+      continue;
     }
-    __syncthreads();
-    const int m = min((uint32_t)kBlendThreads, n - base);
-    if (inside && (!done || count_frags)) {
-      for (int e = 0; e < m; ++e) {
-        float w;
-        if (!entry_weight<MODE, CMAX>(cs, e, px, py, w)) continue;
-        nfrag++;
-        if (done) continue;
-        float alpha = fminf(__fmul_rn(cs.o[e], w), g.amax);
-        float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-        if (Tn < g.tmin) {
-          done = true;
-          continue;
-        }
-        float wgt = alpha * T;
+    const float wgt = alpha * s.T;
+    if (CMAX == 4) {
+      const float4 fv = *reinterpret_cast<const float4*>(&cs.f[e][0]);
+      s.F[0] += wgt * fv.x;
+      s.F[1] += wgt * fv.y;
+      s.F[2] += wgt * fv.z;
+      s.F[3] += wgt * fv.w;
+    } else {
 #pragma unroll
-        for (int c = 0; c < CMAX; ++c)
-          if (c < g.C) Fv[c] += wgt * cs.f[e][c];
-        Dv += wgt * cs.z[e];
-        T = Tn;
-        last = base + e + 1;
-        ncontrib++;
-      }
+      for (int c = 0; c < CMAX; ++c)
+        if (c < g.C) s.F[c] += wgt * cs.f[e][c];
     }
-    if (!count_frags && __syncthreads_and(done)) break;
+    s.D += wgt * cs.z[e];
+    s.T = Tn;
+    s.last = base + e + 1;
+    s.ncontrib++;
   }
-  if (!inside) return;
+}
+
+template <int CMAX>
+__device__ __forceinline__ void write_pixel(const DevCfg& g, const BlendOut& out,
+                                            const float* __restrict__ bg, int px, int py,
+                                            PixFwd<CMAX>& s) {
   const size_t pix = (size_t)py * g.W + px;
   if (bg) {
 #pragma unroll
     for (int c = 0; c < CMAX; ++c)
-      if (c < g.C) Fv[c] += T * __ldg(bg + pix * g.C + c);
+      if (c < g.C) s.F[c] += s.T * __ldg(bg + pix * g.C + c);
   }
   if (CMAX == 4 && g.C == 4) {
-    reinterpret_cast<float4*>(out.F)[pix] = make_float4(Fv[0], Fv[1], Fv[2], Fv[3]);
+    reinterpret_cast<float4*>(out.F)[pix] = make_float4(s.F[0], s.F[1], s.F[2], s.F[3]);
   } else {
 #pragma unroll
     for (int c = 0; c < CMAX; ++c)
-      if (c < g.C) out.F[pix * g.C + c] = Fv[c];
+      if (c < g.C) out.F[pix * g.C + c] = s.F[c];
   }
-  if (out.A) out.A[pix] = 1.0f - T;
-  if (out.D) out.D[pix] = Dv;
-  out.T_final[pix] = T;
-  out.last[pix] = last;
-  if (out.nfrag) out.nfrag[pix] = nfrag;
-  if (out.ncontrib) out.ncontrib[pix] = ncontrib;
+  if (out.A) out.A[pix] = 1.0f - s.T;
+  if (out.D) out.D[pix] = s.D;
+  out.T_final[pix] = s.T;
+  out.last[pix] = s.last;
+  if (out.nfrag) out.nfrag[pix] = s.nfrag;
+  if (out.ncontrib) out.ncontrib[pix] = s.ncontrib;
+}
+
+// ---------------------------------------------------------------- H4/H6 (small tiles) + H7
+// One warp per 8x8 tile; lane l owns pixels (l & 7, l >> 3) and (l & 7, 4 + (l >> 3)).
+template <int MODE, int CMAX>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_fwd(
+    DevCam cam, DevCfg g, int band_tiles, const PointRec* __restrict__ rec,
+    const float* __restrict__ feat, bool packed, const float* __restrict__ bg,
+    const uint32_t* __restrict__ ranges, const unsigned long long* __restrict__ entries,
+    uint32_t* __restrict__ sorted_idx, BlendOut out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  FwdSmem<CMAX>& S = reinterpret_cast<FwdSmem<CMAX>*>(smem_raw)[warp];
+  const int tl = blockIdx.x * kWarpsPerBlock + warp;
+  if (tl >= band_tiles) return;  // warp-uniform; no block barriers below
+  const int tile = g.ty0 * g.tiles_x + tl;
+  const int tx0 = (tile % g.tiles_x) * kTile, ty0 = (tile / g.tiles_x) * kTile;
+  const int px = tx0 + (lane & 7), pyA = ty0 + (lane >> 3), pyB = pyA + 4;
+  const bool inA = px < g.W && pyA < g.H, inB = px < g.W && pyB < g.H;
+  const uint32_t begin = ranges[tile], n = ranges[tile + 1] - begin;
+  const bool small = n <= (uint32_t)kWarpSortCap;
+  if (small && n > 0) {
+    warp_sort(S.keys, entries + begin, (int)n, lane);
+    for (uint32_t k = lane; k < n; k += 32) sorted_idx[begin + k] = (uint32_t)S.keys[k];
+  }
+  const bool count = out.nfrag != nullptr;
+  PixFwd<CMAX> a, b;
+  a.T = b.T = 1.0f;
+  a.D = b.D = 0.0f;
+#pragma unroll
+  for (int c = 0; c < CMAX; ++c) a.F[c] = b.F[c] = 0.0f;
+  a.last = b.last = 0;
+  a.nfrag = b.nfrag = a.ncontrib = b.ncontrib = 0;
+  a.done = !inA;
+  b.done = !inB;
+  ChunkSmem<CMAX>& cs = S.ch;
+  for (uint32_t base = 0; base < n; base += 32) {
+    const uint32_t e = base + lane;
+    cs.mask[lane] = 0u;
+    cs.mask[lane + 32] = 0u;
+    __syncwarp();
+    if (e < n) {
+      const uint32_t idx = small ? (uint32_t)S.keys[e] : __ldg(sorted_idx + begin + e);
+      stage_entry<MODE, CMAX>(cs, lane, g, rec, feat, packed, idx, tx0, ty0);
+    }
+    __syncwarp();
+    blend_pixel<MODE, CMAX>(cs, g, cs.mask[lane], px, pyA, base, count, a);
+    blend_pixel<MODE, CMAX>(cs, g, cs.mask[lane + 32], px, pyB, base, count, b);
+    __syncwarp();
+    if (!count && __all_sync(0xffffffffu, a.done && b.done)) break;
+  }
+  if (inA) write_pixel<CMAX>(g, out, bg, px, pyA, a);
+  if (inB) write_pixel<CMAX>(g, out, bg, px, pyB, b);
 }
 
 // ---------------------------------------------------------------- H8
 struct BwdIn {
-  const float* gF;      // [H,W,C]
-  const float* gA;      // [H,W] or null
-  const float* gD;      // [H,W] or null
-  const float* T_final; // saved
-  const uint32_t* last; // saved
-  float* g_feat;        // [N,C] +=
-  float* g_op;          // [N] +=
+  const float* gF;       // [H,W,C]
+  const float* gA;       // [H,W] or null
+  const float* gD;       // [H,W] or null
+  const float* T_final;  // saved
+  const uint32_t* last;  // saved
+  float* g_feat;         // [N,C] +=
+  float* g_op;           // [N] +=
 };
 
-template <int MODE, int CMAX>
-__global__ void __launch_bounds__(kBlendThreads) k_blend_bwd(
-    DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ feat,
-    const float* __restrict__ opacity, const float* __restrict__ bg,
-    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ sorted_idx, BwdIn in) {
-  __shared__ ChunkSmem<CMAX> cs;
-  __shared__ float acc_f[kBlendThreads][CMAX];
-  __shared__ float acc_o[kBlendThreads];
-  __shared__ int touched[kBlendThreads];
-  __shared__ uint32_t smax;
-  const int tile = g.ty0 * g.tiles_x + blockIdx.x;
-  const int tx = tile % g.tiles_x, ty = tile / g.tiles_x;
-  const int px = tx * kTile + (threadIdx.x & 7), py = ty * kTile + (threadIdx.x >> 3);
-  const bool inside = px < g.W && py < g.H;
-  const uint32_t begin = ranges[tile];
-  const size_t pix = (size_t)py * g.W + px;
-  uint32_t last = 0;
-  float T = 1.0f, GA = 0.0f, GD = 0.0f, RD = 0.0f, P = 1.0f;
+template <int CMAX>
+struct PixBwd {
+  float T, GA, GD, RD, P;
   float G[CMAX], R[CMAX];
+  uint32_t last;
+};
+
+template <int CMAX>
+__device__ __forceinline__ void load_pixel_bwd(const DevCfg& g, const BwdIn& in,
+                                               const float* __restrict__ bg, bool inside, int px,
+                                               int py, PixBwd<CMAX>& s) {
+  s.T = 1.0f;
+  s.GA = s.GD = s.RD = 0.0f;
+  s.P = 1.0f;
+  s.last = 0;
 #pragma unroll
-  for (int c = 0; c < CMAX; ++c) {
-    G[c] = 0.0f;
-    R[c] = 0.0f;
-  }
-  if (inside) {
-    last = in.last[pix];
-    T = in.T_final[pix];
-    if (in.gA) GA = in.gA[pix];
-    if (in.gD) GD = in.gD[pix];
-    if (CMAX == 4 && g.C == 4) {
-      float4 v = __ldg(reinterpret_cast<const float4*>(in.gF) + pix);
-      G[0] = v.x; G[1] = v.y; G[2] = v.z; G[3] = v.w;
-      if (bg) {
-        float4 b = __ldg(reinterpret_cast<const float4*>(bg) + pix);
-        R[0] = b.x; R[1] = b.y; R[2] = b.z; R[3] = b.w;
+  for (int c = 0; c < CMAX; ++c) s.G[c] = s.R[c] = 0.0f;
+  if (!inside) return;
+  const size_t pix = (size_t)py * g.W + px;
+  s.last = in.last[pix];
+  s.T = in.T_final[pix];
+  if (in.gA) s.GA = in.gA[pix];
+  if (in.gD) s.GD = in.gD[pix];
+  if (CMAX == 4 && g.C == 4) {
+    float4 v = __ldg(reinterpret_cast<const float4*>(in.gF) + pix);
+    s.G[0] = v.x; s.G[1] = v.y; s.G[2] = v.z; s.G[3] = v.w;
+    if (bg) {
+      float4 r = __ldg(reinterpret_cast<const float4*>(bg) + pix);
+      s.R[0] = r.x; s.R[1] = r.y; s.R[2] = r.z; s.R[3] = r.w;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c)
+      if (c < g.C) {
+        s.G[c] = in.gF[pix * g.C + c];
+        if (bg) s.R[c] = bg[pix * g.C + c];
       }
+  }
+}
+
+// Reverse-order backward of one pixel over this chunk's fragments (bits of
+// m, descending = reverse list order): T_k recovered as T_{k+1}/(1-alpha_k);
+// dL/dalpha_k = T_k [sum_c G_c (f_c - R_c) + G_D (z - R_D) + G_A P] (Eq. 2
+// corrected, R12); alpha = 0 fragments are processed (R13).
+template <int MODE, int CMAX>
+__device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& g, uint32_t m,
+                                          int px, int py, PixBwd<CMAX>& s) {
+  using SM = BwdSmem<MODE, CMAX>;
+  const ChunkSmem<CMAX>& cs = S.ch;
+  while (m) {
+    const int e = 31 - __clz(m);
+    m &= ~(1u << e);
+    float w;
+    int corner;
+    if (!entry_weight<MODE, CMAX>(cs, e, px, py, w, corner)) continue;
+    const float ow = __fmul_rn(cs.o[e], w);
+    const float alpha = fminf(ow, g.amax);
+    if ((g.flags & kFlagSkipZero) && alpha == 0.0f) continue;
+    const float one_m = __fsub_rn(1.0f, alpha);
+    const float Tk = __fdiv_rn(s.T, one_m);
+    float f[CMAX];
+    float dA = 0.0f;
+    if (CMAX == 4) {
+      const float4 fv = *reinterpret_cast<const float4*>(&cs.f[e][0]);
+      f[0] = fv.x; f[1] = fv.y; f[2] = fv.z; f[3] = fv.w;
+    } else {
+#pragma unroll
+      for (int c = 0; c < CMAX; ++c) f[c] = c < g.C ? cs.f[e][c] : 0.0f;
+    }
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) dA += s.G[c] * (f[c] - s.R[c]);
+    const float z = cs.z[e];
+    dA += s.GD * (z - s.RD) + s.GA * s.P;
+    dA *= Tk;
+    const float ta = Tk * alpha;
+    const float go = ow < g.amax ? w * dA : 0.0f;  // the clamp has zero slope
+    if (SM::kSlots) {
+      float* sl = &S.acc[e][corner * (CMAX + 1)];
+#pragma unroll
+      for (int c = 0; c < CMAX; ++c) sl[c] = ta * s.G[c];
+      sl[CMAX] = go;
     } else {
 #pragma unroll
       for (int c = 0; c < CMAX; ++c)
-        if (c < g.C) {
-          G[c] = in.gF[pix * g.C + c];
-          if (bg) R[c] = bg[pix * g.C + c];
-        }
+        if (c < g.C) atomicAdd(&S.acc[e][c], ta * s.G[c]);
+      atomicAdd(&S.acc[e][CMAX], go);
     }
+    S.touched[e] = 1;
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) s.R[c] = alpha * f[c] + one_m * s.R[c];
+    s.RD = alpha * z + one_m * s.RD;
+    s.P *= one_m;
+    s.T = Tk;
   }
-  if (threadIdx.x == 0) smax = 0;
-  __syncthreads();
-  if (last) atomicMax(&smax, last);
-  __syncthreads();
-  const uint32_t tmax = smax;
+}
+
+__device__ __forceinline__ uint32_t below_mask(uint32_t last, uint32_t base) {
+  // bits e with base + e < last
+  if (last <= base) return 0u;
+  uint32_t k = last - base;
+  return k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
+}
+
+template <int MODE, int CMAX>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_bwd(
+    DevCam cam, DevCfg g, int band_tiles, const PointRec* __restrict__ rec,
+    const float* __restrict__ feat, bool packed, const float* __restrict__ bg,
+    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ sorted_idx, BwdIn in) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  using SM = BwdSmem<MODE, CMAX>;
+  SM& S = reinterpret_cast<SM*>(smem_raw)[warp];
+  const int tl = blockIdx.x * kWarpsPerBlock + warp;
+  if (tl >= band_tiles) return;
+  const int tile = g.ty0 * g.tiles_x + tl;
+  const int tx0 = (tile % g.tiles_x) * kTile, ty0 = (tile / g.tiles_x) * kTile;
+  const int px = tx0 + (lane & 7), pyA = ty0 + (lane >> 3), pyB = pyA + 4;
+  const bool inA = px < g.W && pyA < g.H, inB = px < g.W && pyB < g.H;
+  const uint32_t begin = ranges[tile];
+  PixBwd<CMAX> a, b;
+  load_pixel_bwd<CMAX>(g, in, bg, inA, px, pyA, a);
+  load_pixel_bwd<CMAX>(g, in, bg, inB, px, pyB, b);
+  uint32_t tmax = max(a.last, b.last);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
   if (tmax == 0) return;
-  for (int chunk = (int)((tmax - 1) / kBlendThreads); chunk >= 0; --chunk) {
-    const uint32_t base = (uint32_t)chunk * kBlendThreads;
-    const uint32_t j = base + threadIdx.x;
+  ChunkSmem<CMAX>& cs = S.ch;
+  for (int chunk = (int)((tmax - 1) >> 5); chunk >= 0; --chunk) {
+    const uint32_t base = (uint32_t)chunk * 32;
+    const uint32_t e = base + lane;
+    cs.mask[lane] = 0u;
+    cs.mask[lane + 32] = 0u;
+#pragma unroll
+    for (int c = 0; c < SM::kStride; ++c) S.acc[lane][c] = 0.0f;
+    S.touched[lane] = 0;
+    __syncwarp();
     uint32_t idx = 0;
-    if (j < tmax) {
-      idx = sorted_idx[begin + j];
-      stage_entry<MODE, CMAX>(cs, threadIdx.x, cam, g, xyz, feat, opacity, idx);
-#pragma unroll
-      for (int c = 0; c < CMAX; ++c) acc_f[threadIdx.x][c] = 0.0f;
-      acc_o[threadIdx.x] = 0.0f;
-      touched[threadIdx.x] = 0;
+    if (e < tmax) {
+      idx = __ldg(sorted_idx + begin + e);
+      stage_entry<MODE, CMAX>(cs, lane, g, rec, feat, packed, idx, tx0, ty0);
     }
-    __syncthreads();
-    if (last > base) {
-      const int e_hi = (int)min((uint32_t)kBlendThreads, last - base) - 1;
-      for (int e = e_hi; e >= 0; --e) {
-        float w;
-        if (!entry_weight<MODE, CMAX>(cs, e, px, py, w)) continue;
-        const float ow = __fmul_rn(cs.o[e], w);
-        const float alpha = fminf(ow, g.amax);
-        if ((g.flags & kFlagSkipZero) && alpha == 0.0f) continue;
-        const float one_m = __fsub_rn(1.0f, alpha);
-        const float Tk = __fdiv_rn(T, one_m);
-        float dA = 0.0f;
+    __syncwarp();
+    bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane] & below_mask(a.last, base), px, pyA, a);
+    bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane + 32] & below_mask(b.last, base), px, pyB, b);
+    __syncwarp();
+    if (e < tmax && S.touched[lane]) {
+      float gsum[CMAX + 1];
 #pragma unroll
-        for (int c = 0; c < CMAX; ++c)
-          if (c < g.C) dA += G[c] * (cs.f[e][c] - R[c]);
-        dA += GD * (cs.z[e] - RD) + GA * P;
-        dA *= Tk;
-        const float ta = Tk * alpha;
-#pragma unroll
-        for (int c = 0; c < CMAX; ++c)
-          if (c < g.C) atomicAdd(&acc_f[e][c], ta * G[c]);
-        if (ow < g.amax) atomicAdd(&acc_o[e], w * dA);
-        touched[e] = 1;
-#pragma unroll
-        for (int c = 0; c < CMAX; ++c)
-          if (c < g.C) R[c] = alpha * cs.f[e][c] + one_m * R[c];
-        RD = alpha * cs.z[e] + one_m * RD;
-        P *= one_m;
-        T = Tk;
+      for (int c = 0; c <= CMAX; ++c) {
+        if (SM::kSlots) {
+          gsum[c] = (S.acc[lane][c] + S.acc[lane][(CMAX + 1) + c]) +
+                    (S.acc[lane][2 * (CMAX + 1) + c] + S.acc[lane][3 * (CMAX + 1) + c]);
+        } else {
+          gsum[c] = S.acc[lane][c];
+        }
       }
-    }
-    __syncthreads();
-    if (j < tmax && touched[threadIdx.x]) {
       if (CMAX == 4 && g.C == 4) {
         atomicAdd(reinterpret_cast<float4*>(in.g_feat) + idx,
-                  make_float4(acc_f[threadIdx.x][0], acc_f[threadIdx.x][1], acc_f[threadIdx.x][2],
-                              acc_f[threadIdx.x][3]));
+                  make_float4(gsum[0], gsum[1], gsum[2], gsum[3]));
       } else {
 #pragma unroll
         for (int c = 0; c < CMAX; ++c)
-          if (c < g.C) atomicAdd(in.g_feat + (size_t)idx * g.C + c, acc_f[threadIdx.x][c]);
+          if (c < g.C) atomicAdd(in.g_feat + (size_t)idx * g.C + c, gsum[c]);
       }
-      atomicAdd(in.g_op + idx, acc_o[threadIdx.x]);
+      atomicAdd(in.g_op + idx, gsum[CMAX]);
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 

@@ -58,9 +58,9 @@ struct Foot {
   float ca, cb, cc;
 };
 
-// H2 bilinear (R3).
-__device__ __forceinline__ bool foot_bilinear(const DevCfg& g, const Proj& p, Foot& f) {
-  float ax = __fsub_rn(p.u, 0.5f), ay = __fsub_rn(p.v, 0.5f);
+// H2 bilinear (R3): block floor(u-1/2) + {0,1}.
+__device__ __forceinline__ bool foot_bilinear(const DevCfg& g, float u, float v, Foot& f) {
+  float ax = __fsub_rn(u, 0.5f), ay = __fsub_rn(v, 0.5f);
   if (!(ax >= -1.0f && ax < (float)g.W && ay >= -1.0f && ay < (float)g.H)) return false;
   float flx = floorf(ax), fly = floorf(ay);
   f.fa = __fsub_rn(ax, flx);
@@ -74,15 +74,15 @@ __device__ __forceinline__ bool foot_bilinear(const DevCfg& g, const Proj& p, Fo
   return true;
 }
 
-// H2 Gaussian (R15-R19): isotropic world std s, EWA Jacobian,
-// dilation, 3-sigma bbox.
-__device__ __forceinline__ bool foot_gauss(const DevCam& c, const DevCfg& g, const Proj& p,
-                                           Foot& f) {
-  float a, b, cc;
+// H2 Gaussian, part 1 (R15-R19): conic of the dilated EWA
+// covariance of an isotropic world Gaussian, and its 3-sigma radius.
+__device__ __forceinline__ bool gauss_conic(const DevCam& c, const DevCfg& g, const Proj& p,
+                                            float& ca, float& cb, float& cc, float& r) {
+  float a, b, c2;
   if (g.flags & kFlagSigmaPx) {
     a = __fadd_rn(__fmul_rn(g.sigma, g.sigma), g.dil);
     b = 0.0f;
-    cc = a;
+    c2 = a;
   } else {
     float s = g.sigma > 0.0f ? g.sigma : __fdiv_rn(__fmul_rn(5.0f, c.z_near), fmaxf(c.fx, c.fy));
     float jx = __fdiv_rn(c.fx, p.zc), jy = __fdiv_rn(c.fy, p.zc);
@@ -90,19 +90,23 @@ __device__ __forceinline__ bool foot_gauss(const DevCam& c, const DevCfg& g, con
     a = __fadd_rn(__fmul_rn(s2, __fmul_rn(__fmul_rn(jx, jx), __fadd_rn(1.0f, __fmul_rn(p.xz, p.xz)))),
                   g.dil);
     b = __fmul_rn(s2, __fmul_rn(__fmul_rn(jx, jy), __fmul_rn(p.xz, p.yz)));
-    cc = __fadd_rn(__fmul_rn(s2, __fmul_rn(__fmul_rn(jy, jy), __fadd_rn(1.0f, __fmul_rn(p.yz, p.yz)))),
+    c2 = __fadd_rn(__fmul_rn(s2, __fmul_rn(__fmul_rn(jy, jy), __fadd_rn(1.0f, __fmul_rn(p.yz, p.yz)))),
                    g.dil);
   }
-  float det = __fsub_rn(__fmul_rn(a, cc), __fmul_rn(b, b));
+  float det = __fsub_rn(__fmul_rn(a, c2), __fmul_rn(b, b));
   if (!(det > 0.0f) || !isfinite(det)) return false;
-  f.ca = __fdiv_rn(cc, det);
-  f.cb = __fdiv_rn(-b, det);
-  f.cc = __fdiv_rn(a, det);
-  float mid = __fmul_rn(0.5f, __fadd_rn(a, cc)), hd = __fmul_rn(0.5f, __fsub_rn(a, cc));
+  ca = __fdiv_rn(c2, det);
+  cb = __fdiv_rn(-b, det);
+  cc = __fdiv_rn(a, det);
+  float mid = __fmul_rn(0.5f, __fadd_rn(a, c2)), hd = __fmul_rn(0.5f, __fsub_rn(a, c2));
   float lmax = __fadd_rn(mid, __fsqrt_rn(__fadd_rn(__fmul_rn(hd, hd), __fmul_rn(b, b))));
-  float r = __fmul_rn(3.0f, __fsqrt_rn(lmax));
-  if (!isfinite(r) || !isfinite(f.ca) || !isfinite(f.cb) || !isfinite(f.cc)) return false;
-  float ax = __fsub_rn(p.u, 0.5f), ay = __fsub_rn(p.v, 0.5f);
+  r = __fmul_rn(3.0f, __fsqrt_rn(lmax));
+  return isfinite(r) && isfinite(ca) && isfinite(cb) && isfinite(cc);
+}
+
+// H2 Gaussian, part 2: clipped pixel bbox of radius r around (u, v) (R17).
+__device__ __forceinline__ bool gauss_rect(const DevCfg& g, float u, float v, float r, Foot& f) {
+  float ax = __fsub_rn(u, 0.5f), ay = __fsub_rn(v, 0.5f);
   float xlo = ceilf(__fsub_rn(ax, r)), xhi = floorf(__fadd_rn(ax, r));
   float ylo = ceilf(__fsub_rn(ay, r)), yhi = floorf(__fadd_rn(ay, r));
   if (!(xhi >= 0.0f && xlo <= (float)(g.W - 1) && yhi >= 0.0f && ylo <= (float)(g.H - 1)))
@@ -113,14 +117,6 @@ __device__ __forceinline__ bool foot_gauss(const DevCam& c, const DevCfg& g, con
   f.ylo = ylo < 0.0f ? 0 : (int)ylo;
   f.yhi = yhi > (float)(g.H - 1) ? g.H - 1 : (int)yhi;
   return true;
-}
-
-template <int MODE>
-__device__ __forceinline__ bool point_foot(const DevCam& c, const DevCfg& g, const float* xyz,
-                                           int64_t i, Proj& p, Foot& f) {
-  float X = __ldg(xyz + 3 * i), Y = __ldg(xyz + 3 * i + 1), Z = __ldg(xyz + 3 * i + 2);
-  if (!project_point(c, X, Y, Z, p)) return false;
-  return MODE == 0 ? foot_bilinear(g, p, f) : foot_gauss(c, g, p, f);
 }
 
 // Gaussian Mahalanobis distance of pixel (px, py), pinned order.
