@@ -150,12 +150,20 @@ INPC_API int inpc_debug_export(inpc_ctx* ctx, int32_t view, uint32_t* depth_keys
                       int64_t* F_t_out, void* stream);
 
 /* Per-stage device timing (CUDA events around each stage; adds no sync to
- * the calls).  inpc_ctx_stage_times synchronises the last stream, returns
- * the accumulated milliseconds and launch counts per stage since the last
- * reset, and resets them when reset != 0. */
+ * the calls).  inpc_ctx_stage_times waits for the recorded events, adds
+ * their elapsed milliseconds to per-stage accumulators and returns the
+ * accumulated milliseconds and kernel-launch counts per stage (arrays of n).
+ * flags: INPC_TIMES_RESET zeroes the accumulators after reading;
+ * INPC_TIMES_KEEP_EVENTS keeps the event pairs pending, for calls captured
+ * in a CUDA graph (read again after every replay; launches are counted per
+ * read).  inpc_ctx_forget_events drops pending pairs (after the graph is
+ * destroyed). */
+#define INPC_TIMES_RESET 1
+#define INPC_TIMES_KEEP_EVENTS 2
 INPC_API int inpc_ctx_set_profiling(inpc_ctx* ctx, int enable);
 INPC_API int inpc_ctx_stage_times(inpc_ctx* ctx, float* ms_out, int64_t* launches_out, int32_t n,
-                         int32_t* n_stages, int reset);
+                         int32_t* n_stages, int flags);
+INPC_API int inpc_ctx_forget_events(inpc_ctx* ctx);
 INPC_API const char* inpc_stage_name(int32_t stage);
 
 /* Human-readable text for a status code (for INPC_CUDA: the last CUDA error

@@ -30,6 +30,7 @@ TILE = 8
 
 EXPORTS = ("inpc_ctx_create", "inpc_ctx_destroy", "inpc_rasterize_fwd", "inpc_rasterize_bwd",
            "inpc_debug_export", "inpc_ctx_set_profiling", "inpc_ctx_stage_times",
+           "inpc_ctx_forget_events",
            "inpc_stage_name", "inpc_status_string", "inpc_version")
 
 
@@ -68,6 +69,7 @@ def _load():
     lib.inpc_ctx_set_profiling.argtypes = [P, ct.c_int]
     lib.inpc_ctx_stage_times.argtypes = [P, ct.POINTER(ct.c_float), ct.POINTER(i64), i32,
                                          ct.POINTER(i32), ct.c_int]
+    lib.inpc_ctx_forget_events.argtypes = [P]
     lib.inpc_stage_name.argtypes = [i32]
     lib.inpc_stage_name.restype = ct.c_char_p
     lib.inpc_status_string.argtypes = [ct.c_int]
@@ -235,14 +237,20 @@ class Context:
     def set_profiling(self, on=True):
         _check(lib.inpc_ctx_set_profiling(self._h, 1 if on else 0))
 
-    def stage_times(self, reset=True):
-        """{stage: (ms, launches)} accumulated since the last reset."""
+    def stage_times(self, reset=True, keep_events=False):
+        """{stage: (ms, launches)} accumulated since the last reset.
+        keep_events: the calls were captured in a CUDA graph; read again
+        after the next replay."""
         n = 16
         ms = (ct.c_float * n)()
         la = (ct.c_int64 * n)()
         ns = ct.c_int32()
-        _check(lib.inpc_ctx_stage_times(self._h, ms, la, n, ct.byref(ns), 1 if reset else 0))
+        flags = (1 if reset else 0) | (2 if keep_events else 0)
+        _check(lib.inpc_ctx_stage_times(self._h, ms, la, n, ct.byref(ns), flags))
         return {lib.inpc_stage_name(k).decode(): (ms[k], la[k]) for k in range(ns.value)}
+
+    def forget_events(self):
+        _check(lib.inpc_ctx_forget_events(self._h))
 
 
 _default_ctx = {}

@@ -69,6 +69,7 @@ struct inpc_ctx {
   std::vector<cudaEvent_t> pool;
   double stage_ms[kNumStages] = {};
   int64_t stage_launches[kNumStages] = {};
+  int64_t pending_launches[kNumStages] = {};  // kernel launches behind the pending event pairs
   cudaStream_t last_stream = nullptr;
   uint32_t* host_scalars = nullptr;  // pinned
 };
@@ -154,6 +155,7 @@ struct StageTimer {
   StageTimer(inpc_ctx* ctx, cudaStream_t st, int stage, int launches) : c(ctx), s(st), on(ctx->profiling) {
     c->stage_launches[stage] += launches;
     if (!on) return;
+    c->pending_launches[stage] += launches;
     ep.a = get_event(c);
     ep.b = get_event(c);
     ep.stage = stage;
@@ -353,18 +355,25 @@ int inpc_ctx_set_profiling(inpc_ctx* c, int enable) {
 }
 
 int inpc_ctx_stage_times(inpc_ctx* c, float* ms_out, int64_t* launches_out, int32_t n,
-                         int32_t* n_stages, int reset) {
+                         int32_t* n_stages, int flags) {
   if (!c) return INPC_INVALID_ARG;
   DeviceGuard dg(c->device);
+  const bool reset = (flags & INPC_TIMES_RESET) != 0, keep = (flags & INPC_TIMES_KEEP_EVENTS) != 0;
   for (auto& e : c->pending) {
     cudaEventSynchronize(e.b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e.a, e.b);
     c->stage_ms[e.stage] += ms;
-    c->pool.push_back(e.a);
-    c->pool.push_back(e.b);
+    if (keep) c->stage_launches[e.stage] += c->pending_launches[e.stage];
   }
-  c->pending.clear();
+  if (!keep) {
+    for (auto& e : c->pending) {
+      c->pool.push_back(e.a);
+      c->pool.push_back(e.b);
+    }
+    c->pending.clear();
+    for (int k = 0; k < kNumStages; ++k) c->pending_launches[k] = 0;
+  }
   if (n_stages) *n_stages = kNumStages;
   for (int k = 0; k < n && k < kNumStages; ++k) {
     if (ms_out) ms_out[k] = (float)c->stage_ms[k];
@@ -376,6 +385,18 @@ int inpc_ctx_stage_times(inpc_ctx* c, float* ms_out, int64_t* launches_out, int3
       c->stage_launches[k] = 0;
     }
   }
+  return INPC_OK;
+}
+
+int inpc_ctx_forget_events(inpc_ctx* c) {
+  if (!c) return INPC_INVALID_ARG;
+  DeviceGuard dg(c->device);
+  for (auto& e : c->pending) {
+    c->pool.push_back(e.a);
+    c->pool.push_back(e.b);
+  }
+  c->pending.clear();
+  for (int k = 0; k < kNumStages; ++k) c->pending_launches[k] = 0;
   return INPC_OK;
 }
 

@@ -262,46 +262,67 @@ __device__ __forceinline__ void block_bitonic(unsigned long long* s, int np) {
     }
 }
 
-// Warp-level sort of n <= kWarpSortCap unique 64-bit keys read from src into
-// keys[0..n) (SMEM).  n <= 32: register bitonic over shuffles; otherwise a
-// warp-synchronous SMEM bitonic network.
+// Register bitonic sort of 32*K 64-bit keys held by a warp, element
+// i = 32 r + lane in v[r]: partners at distance j < 32 are exchanged with
+// shuffles, larger distances are register swaps.  Ascending.
+template <int K>
+__device__ __forceinline__ void reg_bitonic(unsigned long long (&v)[K], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * K; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          if ((r & jr) == 0) {
+            const int r2 = r | jr;
+            const bool up = ((r * 32) & k) == 0;
+            const unsigned long long a = v[r], b = v[r2];
+            const bool sw = (a > b) == up;
+            v[r] = sw ? b : a;
+            v[r2] = sw ? a : b;
+          }
+        }
+      } else {
+        const bool lower = (lane & j) == 0;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], j);
+          const bool up = ((r * 32 + lane) & k) == 0;
+          const bool keep_min = lower == up;
+          v[r] = keep_min ? (o < v[r] ? o : v[r]) : (o > v[r] ? o : v[r]);
+        }
+      }
+    }
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void warp_sort_k(unsigned long long* keys,
+                                            const unsigned long long* __restrict__ src, int n,
+                                            int lane) {
+  unsigned long long v[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int i = r * 32 + lane;
+    v[r] = i < n ? src[i] : ~0ull;
+  }
+  reg_bitonic<K>(v, lane);
+#pragma unroll
+  for (int r = 0; r < K; ++r) keys[r * 32 + lane] = v[r];
+  __syncwarp();
+}
+
+// Warp-level sort of n <= kWarpSortCap unique 64-bit (depth key, index)
+// keys read from src into keys[0..n) (SMEM), all in registers.
 __device__ __forceinline__ void warp_sort(unsigned long long* keys,
                                           const unsigned long long* __restrict__ src, int n,
                                           int lane) {
-  if (n <= 32) {
-    unsigned long long v = lane < n ? src[lane] : ~0ull;
-#pragma unroll
-    for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        unsigned long long o = __shfl_xor_sync(0xffffffffu, v, j);
-        bool up = (lane & k) == 0;
-        bool lower = (lane & j) == 0;
-        // lower element keeps min when ascending
-        v = (lower == up) ? (o < v ? o : v) : (o > v ? o : v);
-      }
-    keys[lane] = v;
-    __syncwarp();
-    return;
-  }
-  int np = 64;
-  while (np < n) np <<= 1;
-  for (int k = lane; k < np; k += 32) keys[k] = k < n ? src[k] : ~0ull;
-  __syncwarp();
-  for (int k = 2; k <= np; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = lane; t < (np >> 1); t += 32) {
-        int i = 2 * t - (t & (j - 1));
-        int ixj = i + j;
-        unsigned long long a = keys[i], b = keys[ixj];
-        bool up = (i & k) == 0;
-        if ((a > b) == up) {
-          keys[i] = b;
-          keys[ixj] = a;
-        }
-      }
-      __syncwarp();
-    }
+  if (n <= 32) warp_sort_k<1>(keys, src, n, lane);
+  else if (n <= 64) warp_sort_k<2>(keys, src, n, lane);
+  else if (n <= 128) warp_sort_k<4>(keys, src, n, lane);
+  else warp_sort_k<8>(keys, src, n, lane);
 }
 
 __device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
