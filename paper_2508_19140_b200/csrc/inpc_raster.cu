@@ -54,7 +54,7 @@ struct inpc_ctx {
   int num_sms = 148;
   int big_grid = 0;
   // scratch (shared by views, stream ordered)
-  Buf zeroed, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow;
+  Buf zeroed, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow, slots;
   uint64_t entry_cap = 0;
   std::vector<ViewState> views;
   // saved-state signature
@@ -331,7 +331,7 @@ int inpc_ctx_destroy(inpc_ctx* c) {
   if (!c) return INPC_INVALID_ARG;
   DeviceGuard dg(c->device);
   cudaDeviceSynchronize();
-  for (Buf* b : {&c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries,
+  for (Buf* b : {&c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots,
                  &c->tmp, &c->overflow})
     free_buf(*b);
   for (auto& v : c->views)
@@ -442,6 +442,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   const size_t zero_bytes = count_bytes + (size_t)scan_blocks * 8;
   if ((st = ensure(c->zeroed, zero_bytes, s))) return st;
   if ((st = ensure(c->cursor, (size_t)(T + 1) * 4, s))) return st;
+  if (!gauss && (st = ensure(c->slots, (size_t)(N > 0 ? N : 1) * 16, s))) return st;
   if ((st = ensure(c->big_tiles, (size_t)(T + 1) * 4, s))) return st;
   if ((st = ensure(c->big_elem, (size_t)(T + 2) * 4, s))) return st;
   if ((st = ensure(c->big_chunk, (size_t)(T + 2) * 4, s))) return st;
@@ -480,10 +481,11 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       uint32_t* dt = debug ? (uint32_t*)vs.dbg_tiles.p : nullptr;
       if (gauss)
         k_project_count<1><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N,
-                                                           (PointRec*)vs.rec.p, tc, dk, dt);
+                                                           (PointRec*)vs.rec.p, tc, nullptr, dk, dt);
       else
         k_project_count<0><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N,
-                                                           (PointRec*)vs.rec.p, tc, dk, dt);
+                                                           (PointRec*)vs.rec.p, tc, (uint4*)c->slots.p,
+                                                           dk, dt);
       CK(cudaGetLastError());
     }
     {
@@ -512,9 +514,10 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
                                           (unsigned long long*)c->entries.p, need,
                                           (uint32_t*)c->overflow.p);
       else
-        k_scatter<0><<<nblk, kPointThreads, 0, s>>>(g, (const PointRec*)vs.rec.p, N, (uint32_t*)c->cursor.p,
-                                          (unsigned long long*)c->entries.p, need,
-                                          (uint32_t*)c->overflow.p);
+        k_scatter_slots<<<nblk, kPointThreads, 0, s>>>(g, (const PointRec*)vs.rec.p,
+                                                       (const uint4*)c->slots.p, N,
+                                                       (const uint32_t*)vs.ranges.p,
+                                                       (unsigned long long*)c->entries.p);
       CK(cudaGetLastError());
     }
     if (N > kWarpSortCap) {  // a tile can only exceed the SMEM cap with > cap points

@@ -53,7 +53,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kPointThreads) k_project_count(
     DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ opacity,
     const float* __restrict__ feat, bool pack, int64_t N, PointRec* __restrict__ rec,
-    uint32_t* __restrict__ tile_count, uint32_t* __restrict__ dbg_key,
+    uint32_t* __restrict__ tile_count, uint4* __restrict__ slots, uint32_t* __restrict__ dbg_key,
     uint32_t* __restrict__ dbg_tiles) {
   const int64_t stride = (int64_t)gridDim.x * kPointThreads;
   const int64_t i0 = (int64_t)blockIdx.x * kPointThreads + threadIdx.x;
@@ -97,8 +97,23 @@ __global__ void __launch_bounds__(kPointThreads) k_project_count(
     if (!ok) continue;
     int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
     int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
-    for (int ty = ty_lo; ty <= ty_hi; ++ty)
-      for (int tx = tx_lo; tx <= tx_hi; ++tx) atomicAdd(tile_count + (size_t)ty * g.tiles_x + tx, 1u);
+    if (MODE == 0) {
+      // bilinear: <= 4 tiles, corner c = 2 dy + dx of the tile block; the
+      // slot of each entry in its tile is kept so that the scatter needs no
+      // atomics (k_scatter_slots).  Fixed register indices: the atomics of
+      // all corners are in flight together.
+      uint32_t sl[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int tx = tx_lo + (c & 1), ty = ty_lo + (c >> 1);
+        sl[c] = (tx <= tx_hi && ty <= ty_hi) ? atomicAdd(tile_count + (size_t)ty * g.tiles_x + tx, 1u)
+                                             : 0xFFFFFFFFu;
+      }
+      slots[i] = make_uint4(sl[0], sl[1], sl[2], sl[3]);
+    } else {
+      for (int ty = ty_lo; ty <= ty_hi; ++ty)
+        for (int tx = tx_lo; tx <= tx_hi; ++tx) atomicAdd(tile_count + (size_t)ty * g.tiles_x + tx, 1u);
+    }
   }
 }
 
@@ -239,6 +254,39 @@ __global__ void __launch_bounds__(kPointThreads) k_scatter(
         if (pos < cap) entries[pos] = kv;
         else atomicOr(overflow, 1u);
       }
+  }
+}
+
+// Bilinear H5 without atomics: entry k of point i goes to
+// ranges[tile_k] + slot_k, the slot taken in k_project_count.
+__global__ void __launch_bounds__(kPointThreads) k_scatter_slots(
+    DevCfg g, const PointRec* __restrict__ rec, const uint4* __restrict__ slots, int64_t N,
+    const uint32_t* __restrict__ ranges, unsigned long long* __restrict__ entries) {
+  const int64_t stride = (int64_t)gridDim.x * kPointThreads;
+  const int64_t i0 = (int64_t)blockIdx.x * kPointThreads + threadIdx.x;
+  float4 A[kPPT];
+#pragma unroll
+  for (int k = 0; k < kPPT; ++k) {
+    int64_t i = i0 + k * stride;
+    if (i < N) A[k] = __ldg(&rec[i].a);
+  }
+#pragma unroll
+  for (int k = 0; k < kPPT; ++k) {
+    int64_t i = i0 + k * stride;
+    if (i >= N) break;
+    Foot f;
+    if (!rec_foot<0>(g, A[k], 0.0f, f)) continue;
+    const uint4 s4 = __ldg(slots + i);
+    const uint32_t sl[4] = {s4.x, s4.y, s4.z, s4.w};
+    const unsigned long long kv = ((unsigned long long)__float_as_uint(A[k].z) << 32) | (uint32_t)i;
+    const int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
+    const int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int tx = tx_lo + (c & 1), ty = ty_lo + (c >> 1);
+      if (tx <= tx_hi && ty <= ty_hi)
+        entries[__ldg(ranges + (size_t)ty * g.tiles_x + tx) + sl[c]] = kv;
+    }
   }
 }
 
@@ -453,8 +501,9 @@ __global__ void __launch_bounds__(kBigThreads) k_sort_big(
 //   Gaussian: u, v and the conic; the pixel lane evaluates q and w (R17)
 template <int CMAX>
 struct ChunkSmem {
-  int x0[32], y0[32];
-  float wc[32][4];              // bilinear corner weights
+  int xy[32];                   // bilinear block origin, x0 | y0 << 16
+  float ac[32][4];              // bilinear alpha = min(o w, alpha_max) per block corner
+  float gw[32][4];              // bilinear dalpha/do per corner: w, or 0 where clamped
   float u[32], v[32], ca[32], cb[32], cc[32];  // Gaussian
   float o[32], z[32];
   float f[32][CMAX];
@@ -483,7 +532,7 @@ struct BwdSmem {
 
 // Stage tile-list entry `idx` in slot `lane` and mark its pixels of the tile
 // (origin tx0, ty0) in the chunk masks.
-template <int MODE, int CMAX>
+template <int MODE, int CMAX, bool BWD>
 __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const DevCfg& g,
                                             const PointRec* __restrict__ rec,
                                             const float* __restrict__ feat, bool packed,
@@ -496,12 +545,19 @@ __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const
   cs.o[lane] = A.w;
   cs.z[lane] = A.z;
   if (MODE == 0) {
-    cs.x0[lane] = f.x0;
-    cs.y0[lane] = f.y0;
+    cs.xy[lane] = (f.x0 & 0xFFFF) | (f.y0 << 16);
     const float fa1 = __fsub_rn(1.0f, f.fa), fb1 = __fsub_rn(1.0f, f.fb);
-    *reinterpret_cast<float4*>(&cs.wc[lane][0]) =
-        make_float4(__fmul_rn(fa1, fb1), __fmul_rn(f.fa, fb1), __fmul_rn(fa1, f.fb),
-                    __fmul_rn(f.fa, f.fb));
+    const float w[4] = {__fmul_rn(fa1, fb1), __fmul_rn(f.fa, fb1), __fmul_rn(fa1, f.fb),
+                        __fmul_rn(f.fa, f.fb)};
+    float al[4], gw[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float ow = __fmul_rn(A.w, w[c]);
+      al[c] = fminf(ow, g.amax);
+      gw[c] = ow < g.amax ? w[c] : 0.0f;
+    }
+    *reinterpret_cast<float4*>(&cs.ac[lane][0]) = make_float4(al[0], al[1], al[2], al[3]);
+    if (BWD) *reinterpret_cast<float4*>(&cs.gw[lane][0]) = make_float4(gw[0], gw[1], gw[2], gw[3]);
   } else {
     cs.u[lane] = A.x;
     cs.v[lane] = A.y;
@@ -515,8 +571,8 @@ __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const
     *reinterpret_cast<float4*>(&cs.f[lane][0]) = __ldg(reinterpret_cast<const float4*>(feat) + idx);
   } else {
 #pragma unroll
-    for (int c = 0; c < CMAX; ++c)
-      if (c < g.C) cs.f[lane][c] = __ldg(feat + (size_t)idx * g.C + c);
+    for (int c = 0; c < CMAX; ++c)  // channels >= C are zero so vector reads stay finite
+      cs.f[lane][c] = c < g.C ? __ldg(feat + (size_t)idx * g.C + c) : 0.0f;
   }
   if (!ok) return;
   // footprint rectangle clipped to the tile, tile-local coordinates
@@ -526,20 +582,27 @@ __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const
     for (int xx = xl; xx <= xh; ++xx) atomicOr(&cs.mask[yy * kTile + xx], 1u << lane);
 }
 
-// Fragment weight of staged entry e at pixel (px, py) and its block corner.
-// Bilinear: every pixel of the rectangle is a fragment.  Gaussian: q <= 9.
+// Fragment of staged entry e at pixel (px, py): alpha (R4, R5), dalpha/do
+// (0 where the clamp is active) and the bilinear block corner.  Bilinear:
+// every pixel of the rectangle is a fragment.  Gaussian: q <= 9 (R17).
 template <int MODE, int CMAX>
-__device__ __forceinline__ bool entry_weight(const ChunkSmem<CMAX>& cs, int e, int px, int py,
-                                             float& w, int& corner) {
+__device__ __forceinline__ bool entry_alpha(const ChunkSmem<CMAX>& cs, const DevCfg& g, int e,
+                                            int px, int py, float& alpha, float& gw,
+                                            int& corner) {
   if (MODE == 0) {
-    corner = 2 * (py - cs.y0[e]) + (px - cs.x0[e]);
-    w = cs.wc[e][corner];
+    const int xy = cs.xy[e];
+    corner = 2 * (py - (xy >> 16)) + (px - (int)(short)(xy & 0xFFFF));
+    alpha = cs.ac[e][corner];
+    gw = cs.gw[e][corner];
     return true;
   } else {
     corner = 0;
-    float q = gauss_q(cs.ca[e], cs.cb[e], cs.cc[e], cs.u[e], cs.v[e], px, py);
+    const float q = gauss_q(cs.ca[e], cs.cb[e], cs.cc[e], cs.u[e], cs.v[e], px, py);
     if (!(q <= 9.0f)) return false;
-    w = expf(__fmul_rn(-0.5f, q));
+    const float w = expf(__fmul_rn(-0.5f, q));
+    const float ow = __fmul_rn(cs.o[e], w);
+    alpha = fminf(ow, g.amax);
+    gw = ow < g.amax ? w : 0.0f;
     return true;
   }
 }
@@ -573,12 +636,11 @@ __device__ __forceinline__ void blend_pixel(const ChunkSmem<CMAX>& cs, const Dev
   while (m) {
     const int e = __ffs(m) - 1;
     m &= m - 1;
-    float w;
+    float alpha, gw;
     int corner;
-    if (!entry_weight<MODE, CMAX>(cs, e, px, py, w, corner)) continue;
+    if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, alpha, gw, corner)) continue;
     s.nfrag++;
     if (s.done) continue;
-    const float alpha = fminf(__fmul_rn(cs.o[e], w), g.amax);
     const float Tn = __fmul_rn(s.T, __fsub_rn(1.0f, alpha));
     if (Tn < g.tmin) {
       s.done = true;
@@ -670,7 +732,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_fwd(
     __syncwarp();
     if (e < n) {
       const uint32_t idx = small ? (uint32_t)S.keys[e] : __ldg(sorted_idx + begin + e);
-      stage_entry<MODE, CMAX>(cs, lane, g, rec, feat, packed, idx, tx0, ty0);
+      stage_entry<MODE, CMAX, false>(cs, lane, g, rec, feat, packed, idx, tx0, ty0);
     }
     __syncwarp();
     blend_pixel<MODE, CMAX>(cs, g, cs.mask[lane], px, pyA, base, count, a);
@@ -745,13 +807,14 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
   while (m) {
     const int e = 31 - __clz(m);
     m &= ~(1u << e);
-    float w;
+    float alpha, gw;
     int corner;
-    if (!entry_weight<MODE, CMAX>(cs, e, px, py, w, corner)) continue;
-    const float ow = __fmul_rn(cs.o[e], w);
-    const float alpha = fminf(ow, g.amax);
+    if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, alpha, gw, corner)) continue;
     if ((g.flags & kFlagSkipZero) && alpha == 0.0f) continue;
     const float one_m = __fsub_rn(1.0f, alpha);
+    // T_k = T_{k+1} / (1 - alpha_k), alpha <= alpha_max < 1.  Correctly
+    // rounded: the recovery error grows with the list length, and the fast
+    // 2-ulp division fails the 1e-3 gate on 40k-fragment pixels.
     const float Tk = __fdiv_rn(s.T, one_m);
     float f[CMAX];
     float dA = 0.0f;
@@ -768,7 +831,7 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
     dA += s.GD * (z - s.RD) + s.GA * s.P;
     dA *= Tk;
     const float ta = Tk * alpha;
-    const float go = ow < g.amax ? w * dA : 0.0f;  // the clamp has zero slope
+    const float go = gw * dA;  // dalpha/do = w, or 0 where the clamp is active
     if (SM::kSlots) {
       float* sl = &S.acc[e][corner * (CMAX + 1)];
 #pragma unroll
@@ -832,7 +895,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_bwd(
     uint32_t idx = 0;
     if (e < tmax) {
       idx = __ldg(sorted_idx + begin + e);
-      stage_entry<MODE, CMAX>(cs, lane, g, rec, feat, packed, idx, tx0, ty0);
+      stage_entry<MODE, CMAX, true>(cs, lane, g, rec, feat, packed, idx, tx0, ty0);
     }
     __syncwarp();
     bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane] & below_mask(a.last, base), px, pyA, a);
