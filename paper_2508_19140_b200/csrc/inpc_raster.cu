@@ -102,8 +102,10 @@ struct DeviceGuard {
 
 // Grow-only buffer.  Growing synchronises the stream first (the old buffer
 // may still be in use by enqueued work).
-int ensure(Buf& b, size_t bytes, cudaStream_t s) {
+int ensure(Buf& b, size_t bytes, cudaStream_t s, bool* fresh = nullptr) {
+  if (fresh) *fresh = false;
   if (bytes <= b.bytes && b.p) return INPC_OK;
+  if (fresh) *fresh = true;
   size_t nb = bytes < 256 ? 256 : bytes + bytes / 4;
   if (b.p) {
     cudaStreamSynchronize(s);
@@ -439,8 +441,12 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   // scratch
   const int scan_blocks = (T + kScanTile - 1) / kScanTile;
   const size_t count_bytes = ((size_t)(T + 1) * 4 + 15) / 16 * 16;
-  const size_t zero_bytes = count_bytes + (size_t)scan_blocks * 8;
-  if ((st = ensure(c->zeroed, zero_bytes, s))) return st;
+  // tile counts, look-back state and ScanCtl: zeroed once at allocation;
+  // k_scan_tiles leaves them zero after every call
+  const size_t zero_bytes = count_bytes + (size_t)scan_blocks * 8 + sizeof(ScanCtl);
+  bool fresh = false;
+  if ((st = ensure(c->zeroed, zero_bytes, s, &fresh))) return st;
+  if (fresh) CK(cudaMemsetAsync(c->zeroed.p, 0, c->zeroed.bytes, s));
   if ((st = ensure(c->cursor, (size_t)(T + 1) * 4, s))) return st;
   if (!gauss && (st = ensure(c->slots, (size_t)(N > 0 ? N : 1) * 16, s))) return st;
   if ((st = ensure(c->big_tiles, (size_t)(T + 1) * 4, s))) return st;
@@ -458,7 +464,8 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     if ((st = ensure(vs.ranges, (size_t)(T + 1) * 4, s))) return st;
     if ((st = ensure(vs.T_final, (size_t)P * 4, s))) return st;
     if ((st = ensure(vs.last, (size_t)P * 4, s))) return st;
-    if ((st = ensure(vs.scalars, sizeof(ViewScalars), s))) return st;
+    if ((st = ensure(vs.scalars, sizeof(ViewScalars), s, &fresh))) return st;
+    if (fresh) CK(cudaMemsetAsync(vs.scalars.p, 0, vs.scalars.bytes, s));
     if ((st = ensure(vs.rec, (size_t)(N > 0 ? N : 1) * sizeof(PointRec), s))) return st;
     if (debug && N > 0) {
       if ((st = ensure(vs.dbg_key, (size_t)N * 4, s))) return st;
@@ -468,12 +475,8 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     const float* bg_v = bg ? bg + (size_t)v * bg_view_stride : nullptr;
     uint32_t* tc = (uint32_t*)c->zeroed.p;
     unsigned long long* scan_state = (unsigned long long*)((char*)c->zeroed.p + count_bytes);
+    ScanCtl* scan_ctl = (ScanCtl*)(scan_state + scan_blocks);
     ViewScalars* sc = (ViewScalars*)vs.scalars.p;
-    {
-      StageTimer tm(c, s, kStMemset, 0);
-      CK(cudaMemsetAsync(c->zeroed.p, 0, zero_bytes, s));
-      CK(cudaMemsetAsync(sc, 0, sizeof(ViewScalars), s));
-    }
     const int nblk = (int)((N + (int64_t)kPointThreads * kPPT - 1) / ((int64_t)kPointThreads * kPPT));
     if (N > 0) {
       StageTimer tm(c, s, kStProject, 1);
@@ -492,7 +495,8 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       StageTimer tm(c, s, kStScan, 1);
       k_scan_tiles<<<scan_blocks, kScanThreads, 0, s>>>(T, tc, (uint32_t*)vs.ranges.p,
                                                         (uint32_t*)c->cursor.p,
-                                                        (uint32_t*)c->big_tiles.p, scan_state, sc);
+                                                        (uint32_t*)c->big_tiles.p, scan_state, scan_ctl,
+                                                        sc);
       CK(cudaGetLastError());
     }
     uint64_t need = bound;
@@ -526,7 +530,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       const uint32_t* bt = (const uint32_t*)c->big_tiles.p;
       uint32_t* be = (uint32_t*)c->big_elem.p;
       uint32_t* bc = (uint32_t*)c->big_chunk.p;
-      const ViewScalars* scc = sc;
+      ViewScalars* scc = sc;
       unsigned long long* en = (unsigned long long*)c->entries.p;
       unsigned long long* tp = (unsigned long long*)c->tmp.p;
       uint32_t* si = (uint32_t*)vs.sorted_idx.p;

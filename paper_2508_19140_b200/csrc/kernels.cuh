@@ -130,32 +130,51 @@ __device__ __forceinline__ bool rec_foot(const DevCfg& g, float4 a, float radius
 // before k_scan_tiles).
 struct ViewScalars {
   uint32_t Ft;       // total tile entries
-  uint32_t num_big;  // tiles with more than kWarpSortCap entries
+  uint32_t num_big;  // tiles with more than kWarpSortCap entries (reset by k_sort_big)
   uint32_t max_big;  // largest of them
-  uint32_t ticket;   // scan CTA ticket
+  uint32_t pad;
+};
+
+// Scan bookkeeping, zero on entry and left zero on exit (the last CTA to
+// finish cleans up), so no memset is needed between calls.
+struct ScanCtl {
+  uint32_t ticket;  // CTA order of the look-back
+  uint32_t done;    // CTAs finished
 };
 
 // Decoupled look-back scan (one pass over the counts): each CTA scans
 // kScanTile counts, publishes its aggregate, and adds the prefix found by
 // walking back over its predecessors' published values.
 // state[b] = flag << 32 | value, flag 1 = aggregate, 2 = inclusive prefix.
+// The counts are zeroed as they are consumed (ready for the next call).
 __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
-    int T, const uint32_t* __restrict__ count, uint32_t* __restrict__ ranges,
+    int T, uint32_t* __restrict__ count, uint32_t* __restrict__ ranges,
     uint32_t* __restrict__ cursor, uint32_t* __restrict__ big_tiles,
-    unsigned long long* state, ViewScalars* sc) {
+    unsigned long long* state, ScanCtl* ctl, ViewScalars* sc) {
   __shared__ uint32_t warp_tot[kScanThreads / 32];
   __shared__ uint32_t s_prefix, s_bid;
-  if (threadIdx.x == 0) s_bid = atomicAdd(&sc->ticket, 1u);
+  if (threadIdx.x == 0) s_bid = atomicAdd(&ctl->ticket, 1u);
   __syncthreads();
   const uint32_t bid = s_bid;
   const int i0 = bid * kScanTile + threadIdx.x * kScanItems;
   uint32_t c[kScanItems];
   uint32_t sum = 0, mx = 0;
+  if (i0 + kScanItems <= T) {
+    uint4* p = reinterpret_cast<uint4*>(count + i0);
+    const uint4 a = p[0], b = p[1];
+    p[0] = make_uint4(0u, 0u, 0u, 0u);
+    p[1] = make_uint4(0u, 0u, 0u, 0u);
+    c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
+    c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+  } else {
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    c[k] = (i0 + k < T) ? count[i0 + k] : 0u;
-    sum += c[k];
+    for (int k = 0; k < kScanItems; ++k) {
+      c[k] = (i0 + k < T) ? count[i0 + k] : 0u;
+      if (i0 + k < T) count[i0 + k] = 0u;
+    }
   }
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) sum += c[k];
   // block exclusive scan of the per-thread sums
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t x = sum;
@@ -218,6 +237,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
   if (i0 < T && i0 + kScanItems >= T) {  // the thread owning the last tile
     ranges[T] = off;
     sc->Ft = off;
+  }
+  // the last CTA to finish leaves the look-back state zero for the next call
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_bid = atomicAdd(&ctl->done, 1u);
+  }
+  __syncthreads();
+  if (s_bid == gridDim.x - 1) {
+    for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) state[b] = 0ull;
+    if (threadIdx.x == 0) {
+      ctl->ticket = 0u;
+      ctl->done = 0u;
+    }
   }
 }
 
@@ -401,7 +434,7 @@ __device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a,
 // synchronised between phases; returns at once if no tile is big.
 __global__ void __launch_bounds__(kBigThreads) k_sort_big(
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles,
-    uint32_t* big_elem, uint32_t* big_chunk, const ViewScalars* sc,
+    uint32_t* big_elem, uint32_t* big_chunk, ViewScalars* sc,
     unsigned long long* entries, unsigned long long* tmp, uint32_t* __restrict__ sorted_idx) {
   namespace cg = cooperative_groups;
   const uint32_t nb = sc->num_big;
@@ -489,6 +522,11 @@ __global__ void __launch_bounds__(kBigThreads) k_sort_big(
     uint32_t begin = ranges[big_tiles[j]];
     uint32_t pos = e - big_elem[j];
     sorted_idx[begin + pos] = (uint32_t)src[begin + pos];
+  }
+  grid.sync();  // everybody has read the big-tile counters: zero them for the next call
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->num_big = 0u;
+    sc->max_big = 0u;
   }
 }
 
