@@ -542,6 +542,7 @@ struct ChunkSmem {
   int xy[32];                   // bilinear block origin, x0 | y0 << 16
   float ac[32][4];              // bilinear alpha = min(o w, alpha_max) per block corner
   float gw[32][4];              // bilinear dalpha/do per corner: w, or 0 where clamped
+  float rc[32][4];              // bilinear 1 / (1 - alpha) per corner (backward)
   float u[32], v[32], ca[32], cb[32], cc[32];  // Gaussian
   float o[32], z[32];
   float f[32][CMAX];
@@ -595,7 +596,12 @@ __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const
       gw[c] = ow < g.amax ? w[c] : 0.0f;
     }
     *reinterpret_cast<float4*>(&cs.ac[lane][0]) = make_float4(al[0], al[1], al[2], al[3]);
-    if (BWD) *reinterpret_cast<float4*>(&cs.gw[lane][0]) = make_float4(gw[0], gw[1], gw[2], gw[3]);
+    if (BWD) {
+      *reinterpret_cast<float4*>(&cs.gw[lane][0]) = make_float4(gw[0], gw[1], gw[2], gw[3]);
+      *reinterpret_cast<float4*>(&cs.rc[lane][0]) =
+          make_float4(__frcp_rn(__fsub_rn(1.0f, al[0])), __frcp_rn(__fsub_rn(1.0f, al[1])),
+                      __frcp_rn(__fsub_rn(1.0f, al[2])), __frcp_rn(__fsub_rn(1.0f, al[3])));
+    }
   } else {
     cs.u[lane] = A.x;
     cs.v[lane] = A.y;
@@ -850,10 +856,14 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
     if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, alpha, gw, corner)) continue;
     if ((g.flags & kFlagSkipZero) && alpha == 0.0f) continue;
     const float one_m = __fsub_rn(1.0f, alpha);
-    // T_k = T_{k+1} / (1 - alpha_k), alpha <= alpha_max < 1.  Correctly
-    // rounded: the recovery error grows with the list length, and the fast
-    // 2-ulp division fails the 1e-3 gate on 40k-fragment pixels.
-    const float Tk = __fdiv_rn(s.T, one_m);
+    // T_k = T_{k+1} / (1 - alpha_k), 0 <= alpha <= alpha_max < 1: quotient
+    // from the staged reciprocal plus one Newton correction of the residual
+    // (as accurate as the IEEE division on this range, without its
+    // special-case branch).  The recovery error grows with the list length;
+    // the plain 2-ulp fast division fails the 1e-3 gate on 40k-fragment pixels.
+    const float rcp = MODE == 0 ? cs.rc[e][corner] : __frcp_rn(one_m);
+    const float q0 = s.T * rcp;
+    const float Tk = fmaf(fmaf(-q0, one_m, s.T), rcp, q0);
     float f[CMAX];
     float dA = 0.0f;
     if (CMAX == 4) {
