@@ -556,28 +556,51 @@ struct FwdSmem {
   ChunkSmem<CMAX> ch;
 };
 
-// Backward per-warp SMEM.  Bilinear with CMAX <= 8: every fragment of an
-// entry in the tile is one of its 2x2 block corners, so each fragment owns a
-// slot [entry][corner] and the per-point sums need no SMEM atomics (float
-// atomicAdd on SMEM is a CAS loop on this part).  Otherwise SMEM atomics.
+// Backward per-warp SMEM.  The pixel's upstream gradient G is staged per
+// tile (Gs), so a fragment only needs two scalars: ta = T_k alpha_k
+// (dL/df_k = ta G) and go = dL/do contribution.  Bilinear: every fragment of
+// an entry in the tile is one of its 2x2 block corners, so each fragment
+// owns a slot [entry][corner] and the entry lane sums its <= 4 corners with
+// no SMEM atomics (float atomicAdd on SMEM is a CAS loop on this part).
+// Gaussian: the pixel lane adds ta G and go to the entry with SMEM atomics.
 template <int MODE, int CMAX>
 struct BwdSmem {
-  static constexpr bool kSlots = MODE == 0 && CMAX <= 8;
-  static constexpr int kStride = kSlots ? 4 * (CMAX + 1) + 1 : CMAX + 2;  // odd: no bank conflicts
+  static constexpr bool kSlots = MODE == 0;
+  static constexpr int kStride = kSlots ? 9 : CMAX + 2;  // odd: no bank conflicts
   ChunkSmem<CMAX> ch;
+  float Gs[64][CMAX];
   float acc[32][kStride];
   int touched[32];
 };
 
-// Stage tile-list entry `idx` in slot `lane` and mark its pixels of the tile
+// The global loads of one tile-list entry, issued a chunk ahead of their
+// use (software pipelining: the warp works on chunk k while chunk k+1's
+// record gathers are in flight).
+struct EntryRegs {
+  float4 A, B, F;  // record halves; F = features when they are not packed
+  uint32_t idx;
+};
+
+template <int CMAX>
+__device__ __forceinline__ EntryRegs load_entry(const DevCfg& g, const PointRec* __restrict__ rec,
+                                                const float* __restrict__ feat, bool packed,
+                                                uint32_t idx) {
+  EntryRegs r;
+  r.idx = idx;
+  r.A = __ldg(&rec[idx].a);
+  r.B = __ldg(&rec[idx].b);
+  if (CMAX == 4 && !packed && g.C == 4) r.F = __ldg(reinterpret_cast<const float4*>(feat) + idx);
+  return r;
+}
+
+// Stage a loaded entry in slot `lane` and mark its pixels of the tile
 // (origin tx0, ty0) in the chunk masks.
 template <int MODE, int CMAX, bool BWD>
 __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const DevCfg& g,
-                                            const PointRec* __restrict__ rec,
-                                            const float* __restrict__ feat, bool packed,
-                                            uint32_t idx, int tx0, int ty0) {
-  const float4 A = __ldg(&rec[idx].a);
-  const float4 B = __ldg(&rec[idx].b);
+                                            const EntryRegs& r, const float* __restrict__ feat,
+                                            bool packed, int tx0, int ty0) {
+  const float4 A = r.A, B = r.B;
+  const uint32_t idx = r.idx;
   Foot f;
   bool ok = rec_foot<MODE>(g, A, B.w, f);
   cs.idx[lane] = idx;
@@ -612,7 +635,7 @@ __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const
   if (CMAX == 4 && packed) {
     *reinterpret_cast<float4*>(&cs.f[lane][0]) = B;
   } else if (CMAX == 4 && g.C == 4) {
-    *reinterpret_cast<float4*>(&cs.f[lane][0]) = __ldg(reinterpret_cast<const float4*>(feat) + idx);
+    *reinterpret_cast<float4*>(&cs.f[lane][0]) = r.F;
   } else {
 #pragma unroll
     for (int c = 0; c < CMAX; ++c)  // channels >= C are zero so vector reads stay finite
@@ -769,14 +792,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_fwd(
   a.done = !inA;
   b.done = !inB;
   ChunkSmem<CMAX>& cs = S.ch;
+  auto idx_at = [&](uint32_t e) -> uint32_t {
+    return small ? (uint32_t)S.keys[e] : __ldg(sorted_idx + begin + e);
+  };
   for (uint32_t base = 0; base < n; base += 32) {
     const uint32_t e = base + lane;
     cs.mask[lane] = 0u;
     cs.mask[lane + 32] = 0u;
     __syncwarp();
     if (e < n) {
-      const uint32_t idx = small ? (uint32_t)S.keys[e] : __ldg(sorted_idx + begin + e);
-      stage_entry<MODE, CMAX, false>(cs, lane, g, rec, feat, packed, idx, tx0, ty0);
+      const EntryRegs r = load_entry<CMAX>(g, rec, feat, packed, idx_at(e));
+      stage_entry<MODE, CMAX, false>(cs, lane, g, r, feat, packed, tx0, ty0);
     }
     __syncwarp();
     blend_pixel<MODE, CMAX>(cs, g, cs.mask[lane], px, pyA, base, count, a);
@@ -801,48 +827,55 @@ struct BwdIn {
 
 template <int CMAX>
 struct PixBwd {
-  float T, GA, GD, RD, P;
-  float G[CMAX], R[CMAX];
+  float T, GA, GD, S, SD, P;  // S = G . R (R: everything behind, normalised), SD likewise for depth
+  float G[CMAX];
   uint32_t last;
 };
 
-template <int CMAX>
+template <int MODE, int CMAX>
 __device__ __forceinline__ void load_pixel_bwd(const DevCfg& g, const BwdIn& in,
                                                const float* __restrict__ bg, bool inside, int px,
-                                               int py, PixBwd<CMAX>& s) {
+                                               int py, float* Gs, PixBwd<CMAX>& s) {
   s.T = 1.0f;
-  s.GA = s.GD = s.RD = 0.0f;
+  s.GA = s.GD = s.S = s.SD = 0.0f;
   s.P = 1.0f;
   s.last = 0;
 #pragma unroll
-  for (int c = 0; c < CMAX; ++c) s.G[c] = s.R[c] = 0.0f;
-  if (!inside) return;
-  const size_t pix = (size_t)py * g.W + px;
-  s.last = in.last[pix];
-  s.T = in.T_final[pix];
-  if (in.gA) s.GA = in.gA[pix];
-  if (in.gD) s.GD = in.gD[pix];
-  if (CMAX == 4 && g.C == 4) {
-    float4 v = __ldg(reinterpret_cast<const float4*>(in.gF) + pix);
-    s.G[0] = v.x; s.G[1] = v.y; s.G[2] = v.z; s.G[3] = v.w;
-    if (bg) {
-      float4 r = __ldg(reinterpret_cast<const float4*>(bg) + pix);
-      s.R[0] = r.x; s.R[1] = r.y; s.R[2] = r.z; s.R[3] = r.w;
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < CMAX; ++c)
-      if (c < g.C) {
-        s.G[c] = in.gF[pix * g.C + c];
-        if (bg) s.R[c] = bg[pix * g.C + c];
+  for (int c = 0; c < CMAX; ++c) s.G[c] = 0.0f;
+  if (inside) {
+    const size_t pix = (size_t)py * g.W + px;
+    s.last = in.last[pix];
+    s.T = in.T_final[pix];
+    if (in.gA) s.GA = in.gA[pix];
+    if (in.gD) s.GD = in.gD[pix];
+    if (CMAX == 4 && g.C == 4) {
+      float4 v = __ldg(reinterpret_cast<const float4*>(in.gF) + pix);
+      s.G[0] = v.x; s.G[1] = v.y; s.G[2] = v.z; s.G[3] = v.w;
+      if (bg) {  // S starts as G . bg: the background is behind every fragment
+        float4 r = __ldg(reinterpret_cast<const float4*>(bg) + pix);
+        s.S = (v.x * r.x + v.y * r.y) + (v.z * r.z + v.w * r.w);
       }
+    } else {
+#pragma unroll
+      for (int c = 0; c < CMAX; ++c)
+        if (c < g.C) {
+          s.G[c] = in.gF[pix * g.C + c];
+          if (bg) s.S += s.G[c] * bg[pix * g.C + c];
+        }
+    }
   }
+#pragma unroll
+  for (int c = 0; c < CMAX; ++c) Gs[c] = s.G[c];
 }
 
 // Reverse-order backward of one pixel over this chunk's fragments (bits of
-// m, descending = reverse list order): T_k recovered as T_{k+1}/(1-alpha_k);
-// dL/dalpha_k = T_k [sum_c G_c (f_c - R_c) + G_D (z - R_D) + G_A P] (Eq. 2
-// corrected, R12); alpha = 0 fragments are processed (R13).
+// m, descending = reverse list order):
+//   T_k = T_{k+1} / (1 - alpha_k)
+//   dL/dalpha_k = T_k [G.f_k - S_k + G_D (z_k - SD_k) + G_A P_k]   (Eq. 2 corrected, R12)
+//   dL/df_k = T_k alpha_k G ;  dL/do += w_k dL/dalpha_k (0 where clamped)
+//   S <- alpha G.f_k + (1 - alpha) S, SD likewise with z, P <- (1 - alpha) P
+// where S = G . R carries the composited colour behind fragment k (R starts
+// as the background).  alpha = 0 fragments are processed (R13).
 template <int MODE, int CMAX>
 __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& g, uint32_t m,
                                           int px, int py, PixBwd<CMAX>& s) {
@@ -856,35 +889,29 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
     if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, alpha, gw, corner)) continue;
     if ((g.flags & kFlagSkipZero) && alpha == 0.0f) continue;
     const float one_m = __fsub_rn(1.0f, alpha);
-    // T_k = T_{k+1} / (1 - alpha_k), 0 <= alpha <= alpha_max < 1: quotient
-    // from the staged reciprocal plus one Newton correction of the residual
-    // (as accurate as the IEEE division on this range, without its
-    // special-case branch).  The recovery error grows with the list length;
-    // the plain 2-ulp fast division fails the 1e-3 gate on 40k-fragment pixels.
+    // T_k from the staged reciprocal plus one Newton correction of the
+    // residual (as accurate as the IEEE division on 0 <= alpha < 1, without
+    // its special-case branch).  The recovery error grows with the list
+    // length; the plain 2-ulp fast division fails the 1e-3 gate on
+    // 40k-fragment pixels.
     const float rcp = MODE == 0 ? cs.rc[e][corner] : __frcp_rn(one_m);
     const float q0 = s.T * rcp;
     const float Tk = fmaf(fmaf(-q0, one_m, s.T), rcp, q0);
-    float f[CMAX];
-    float dA = 0.0f;
+    float gf = 0.0f;
     if (CMAX == 4) {
       const float4 fv = *reinterpret_cast<const float4*>(&cs.f[e][0]);
-      f[0] = fv.x; f[1] = fv.y; f[2] = fv.z; f[3] = fv.w;
+      gf = (s.G[0] * fv.x + s.G[1] * fv.y) + (s.G[2] * fv.z + s.G[3] * fv.w);
     } else {
 #pragma unroll
-      for (int c = 0; c < CMAX; ++c) f[c] = c < g.C ? cs.f[e][c] : 0.0f;
+      for (int c = 0; c < CMAX; ++c) gf += s.G[c] * cs.f[e][c];
     }
-#pragma unroll
-    for (int c = 0; c < CMAX; ++c) dA += s.G[c] * (f[c] - s.R[c]);
     const float z = cs.z[e];
-    dA += s.GD * (z - s.RD) + s.GA * s.P;
-    dA *= Tk;
+    const float dA = Tk * ((gf - s.S) + s.GD * (z - s.SD) + s.GA * s.P);
     const float ta = Tk * alpha;
     const float go = gw * dA;  // dalpha/do = w, or 0 where the clamp is active
     if (SM::kSlots) {
-      float* sl = &S.acc[e][corner * (CMAX + 1)];
-#pragma unroll
-      for (int c = 0; c < CMAX; ++c) sl[c] = ta * s.G[c];
-      sl[CMAX] = go;
+      S.acc[e][2 * corner] = ta;  // odd row stride: scalar stores
+      S.acc[e][2 * corner + 1] = go;
     } else {
 #pragma unroll
       for (int c = 0; c < CMAX; ++c)
@@ -892,9 +919,8 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
       atomicAdd(&S.acc[e][CMAX], go);
     }
     S.touched[e] = 1;
-#pragma unroll
-    for (int c = 0; c < CMAX; ++c) s.R[c] = alpha * f[c] + one_m * s.R[c];
-    s.RD = alpha * z + one_m * s.RD;
+    s.S = alpha * gf + one_m * s.S;
+    s.SD = alpha * z + one_m * s.SD;
     s.P *= one_m;
     s.T = Tk;
   }
@@ -924,8 +950,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_bwd(
   const bool inA = px < g.W && pyA < g.H, inB = px < g.W && pyB < g.H;
   const uint32_t begin = ranges[tile];
   PixBwd<CMAX> a, b;
-  load_pixel_bwd<CMAX>(g, in, bg, inA, px, pyA, a);
-  load_pixel_bwd<CMAX>(g, in, bg, inB, px, pyB, b);
+  load_pixel_bwd<MODE, CMAX>(g, in, bg, inA, px, pyA, &S.Gs[lane][0], a);
+  load_pixel_bwd<MODE, CMAX>(g, in, bg, inB, px, pyB, &S.Gs[lane + 32][0], b);
   uint32_t tmax = max(a.last, b.last);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
@@ -943,7 +969,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_bwd(
     uint32_t idx = 0;
     if (e < tmax) {
       idx = __ldg(sorted_idx + begin + e);
-      stage_entry<MODE, CMAX, true>(cs, lane, g, rec, feat, packed, idx, tx0, ty0);
+      const EntryRegs r = load_entry<CMAX>(g, rec, feat, packed, idx);
+      stage_entry<MODE, CMAX, true>(cs, lane, g, r, feat, packed, tx0, ty0);
     }
     __syncwarp();
     bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane] & below_mask(a.last, base), px, pyA, a);
@@ -952,13 +979,24 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_bwd(
     if (e < tmax && S.touched[lane]) {
       float gsum[CMAX + 1];
 #pragma unroll
-      for (int c = 0; c <= CMAX; ++c) {
-        if (SM::kSlots) {
-          gsum[c] = (S.acc[lane][c] + S.acc[lane][(CMAX + 1) + c]) +
-                    (S.acc[lane][2 * (CMAX + 1) + c] + S.acc[lane][3 * (CMAX + 1) + c]);
-        } else {
-          gsum[c] = S.acc[lane][c];
+      for (int c = 0; c <= CMAX; ++c) gsum[c] = 0.0f;
+      if (SM::kSlots) {
+        // corner k of the block is tile pixel (x0 + (k & 1), y0 + (k >> 1))
+        const int xy = cs.xy[lane];
+        const int lx = (int)(short)(xy & 0xFFFF) - tx0, ly = (xy >> 16) - ty0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int cx = lx + (k & 1), cy = ly + (k >> 1);
+          if (cx < 0 || cx >= kTile || cy < 0 || cy >= kTile) continue;
+          const float2 sl = make_float2(S.acc[lane][2 * k], S.acc[lane][2 * k + 1]);
+          const float* Gp = &S.Gs[cy * kTile + cx][0];
+#pragma unroll
+          for (int c = 0; c < CMAX; ++c) gsum[c] += sl.x * Gp[c];
+          gsum[CMAX] += sl.y;
         }
+      } else {
+#pragma unroll
+        for (int c = 0; c <= CMAX; ++c) gsum[c] = S.acc[lane][c];
       }
       if (CMAX == 4 && g.C == 4) {
         atomicAdd(reinterpret_cast<float4*>(in.g_feat) + idx,
