@@ -230,17 +230,31 @@ void set_smem(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+template <int MODE, int CMAX, bool COUNT>
+void launch_blend_fwd_t(int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
+                        const PointRec* rec, const float* feat, bool packed, const float* bg,
+                        const uint32_t* ranges, const unsigned long long* entries,
+                        uint32_t* sorted_idx, const BlendOut& o) {
+  const size_t smem = kWarpsPerBlock * sizeof(FwdSmem<CMAX>);
+  static bool once = (set_smem(k_blend_fwd<MODE, CMAX, COUNT>, smem), true);
+  (void)once;
+  const int grid = (band_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  k_blend_fwd<MODE, CMAX, COUNT><<<grid, kWarpsPerBlock * 32, smem, s>>>(
+      dc, g, band_tiles, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
+}
+
 template <int MODE, int CMAX>
 void launch_blend_fwd(int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
                       const PointRec* rec, const float* feat, bool packed, const float* bg,
                       const uint32_t* ranges, const unsigned long long* entries,
                       uint32_t* sorted_idx, const BlendOut& o) {
-  const size_t smem = kWarpsPerBlock * sizeof(FwdSmem<CMAX>);
-  static bool once = (set_smem(k_blend_fwd<MODE, CMAX>, smem), true);
-  (void)once;
-  const int grid = (band_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  k_blend_fwd<MODE, CMAX><<<grid, kWarpsPerBlock * 32, smem, s>>>(dc, g, band_tiles, rec, feat, packed,
-                                                                  bg, ranges, entries, sorted_idx, o);
+  // the debug counts (n_frag, n_contrib) need every fragment visited
+  if (o.nfrag || o.ncontrib)
+    launch_blend_fwd_t<MODE, CMAX, true>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries,
+                                         sorted_idx, o);
+  else
+    launch_blend_fwd_t<MODE, CMAX, false>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries,
+                                          sorted_idx, o);
 }
 
 template <int MODE, int CMAX>

@@ -695,10 +695,11 @@ struct PixFwd {
 
 // Composite the fragments of one pixel in this chunk (bits of m, ascending =
 // list order), Eq. 1 with alpha clamp (R5) and early termination (R6).
-template <int MODE, int CMAX>
+template <int MODE, int CMAX, bool COUNT>
 __device__ __forceinline__ void blend_pixel(const ChunkSmem<CMAX>& cs, const DevCfg& g,
                                             uint32_t m, int px, int py, uint32_t base,
-                                            bool count, PixFwd<CMAX>& s) {
+                                            PixFwd<CMAX>& s) {
+  const bool count = COUNT;
   if (s.done && !count) return;
   while (m) {
     const int e = __ffs(m) - 1;
@@ -706,7 +707,7 @@ __device__ __forceinline__ void blend_pixel(const ChunkSmem<CMAX>& cs, const Dev
     float alpha, gw;
     int corner;
     if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, alpha, gw, corner)) continue;
-    s.nfrag++;
+    if (COUNT) s.nfrag++;
     if (s.done) continue;
     const float Tn = __fmul_rn(s.T, __fsub_rn(1.0f, alpha));
     if (Tn < g.tmin) {
@@ -729,7 +730,7 @@ __device__ __forceinline__ void blend_pixel(const ChunkSmem<CMAX>& cs, const Dev
     s.D += wgt * cs.z[e];
     s.T = Tn;
     s.last = base + e + 1;
-    s.ncontrib++;
+    if (COUNT) s.ncontrib++;
   }
 }
 
@@ -754,13 +755,13 @@ __device__ __forceinline__ void write_pixel(const DevCfg& g, const BlendOut& out
   if (out.D) out.D[pix] = s.D;
   out.T_final[pix] = s.T;
   out.last[pix] = s.last;
-  if (out.nfrag) out.nfrag[pix] = s.nfrag;
+  if (out.nfrag) out.nfrag[pix] = s.nfrag;      // set only in COUNT mode
   if (out.ncontrib) out.ncontrib[pix] = s.ncontrib;
 }
 
 // ---------------------------------------------------------------- H4/H6 (small tiles) + H7
 // One warp per 8x8 tile; lane l owns pixels (l & 7, l >> 3) and (l & 7, 4 + (l >> 3)).
-template <int MODE, int CMAX>
+template <int MODE, int CMAX, bool COUNT>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_fwd(
     DevCam cam, DevCfg g, int band_tiles, const PointRec* __restrict__ rec,
     const float* __restrict__ feat, bool packed, const float* __restrict__ bg,
@@ -781,7 +782,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_fwd(
     warp_sort(S.keys, entries + begin, (int)n, lane);
     for (uint32_t k = lane; k < n; k += 32) sorted_idx[begin + k] = (uint32_t)S.keys[k];
   }
-  const bool count = out.nfrag != nullptr;
+  const bool count = COUNT;  // debug counts (n_frag, n_contrib): no early exit
   PixFwd<CMAX> a, b;
   a.T = b.T = 1.0f;
   a.D = b.D = 0.0f;
@@ -805,8 +806,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_fwd(
       stage_entry<MODE, CMAX, false>(cs, lane, g, r, feat, packed, tx0, ty0);
     }
     __syncwarp();
-    blend_pixel<MODE, CMAX>(cs, g, cs.mask[lane], px, pyA, base, count, a);
-    blend_pixel<MODE, CMAX>(cs, g, cs.mask[lane + 32], px, pyB, base, count, b);
+    blend_pixel<MODE, CMAX, COUNT>(cs, g, cs.mask[lane], px, pyA, base, a);
+    blend_pixel<MODE, CMAX, COUNT>(cs, g, cs.mask[lane + 32], px, pyB, base, b);
     __syncwarp();
     if (!count && __all_sync(0xffffffffu, a.done && b.done)) break;
   }
