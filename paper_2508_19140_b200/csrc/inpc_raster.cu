@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -32,10 +33,11 @@ enum Stage : int {
   kStSortBig,
   kStBlendFwd,
   kStBlendBwd,
+  kStBin,
   kNumStages
 };
 const char* kStageNames[kNumStages] = {"memset", "project_count", "scan_tiles", "scatter",
-                                       "sort_big", "blend_fwd", "blend_bwd"};
+                                       "sort_big", "blend_fwd", "blend_bwd", "bin_fused"};
 
 struct ViewState {
   Buf ranges, sorted_idx, T_final, last, dbg_key, dbg_tiles, scalars, rec;
@@ -54,7 +56,9 @@ struct inpc_ctx {
   int num_sms = 148;
   int big_grid = 0;
   // scratch (shared by views, stream ordered)
-  Buf zeroed, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow, slots;
+  Buf zeroed, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg;
+  int bin_grid[3] = {0, 0, 0};  // cooperative grid of k_bin_bilinear<2,4,8>
+  bool no_fused_bin = false;     // env INPC_NO_FUSED_BIN=1: separate binning kernels
   uint64_t entry_cap = 0;
   std::vector<ViewState> views;
   // saved-state signature
@@ -334,6 +338,19 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_big, kBigThreads, 0);
   c->big_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
+  {
+    int o2 = 0, o4 = 0, o8 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_bin_bilinear<2>, kBinThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k_bin_bilinear<4>, kBinThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o8, k_bin_bilinear<8>, kBinThreads, 0);
+    c->bin_grid[0] = c->num_sms * o2;
+    c->bin_grid[1] = c->num_sms * o4;
+    c->bin_grid[2] = c->num_sms * o8;
+  }
+  {
+    const char* e = getenv("INPC_NO_FUSED_BIN");
+    c->no_fused_bin = e && e[0] == '1';
+  }
   if (cudaMallocHost(&c->host_scalars, 64) != cudaSuccess) {
     cudaGetLastError();
     delete c;
@@ -347,7 +364,7 @@ int inpc_ctx_destroy(inpc_ctx* c) {
   if (!c) return INPC_INVALID_ARG;
   DeviceGuard dg(c->device);
   cudaDeviceSynchronize();
-  for (Buf* b : {&c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots,
+  for (Buf* b : {&c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots, &c->agg,
                  &c->tmp, &c->overflow})
     free_buf(*b);
   for (auto& v : c->views)
@@ -492,10 +509,54 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     ScanCtl* scan_ctl = (ScanCtl*)(scan_state + scan_blocks);
     ViewScalars* sc = (ViewScalars*)vs.scalars.p;
     const int nblk = (int)((N + (int64_t)kPointThreads * kPPT - 1) / ((int64_t)kPointThreads * kPPT));
-    if (N > 0) {
+    // bilinear: one cooperative launch for H1-H6 when the points fit in registers
+    // (measured on cfg 2: the fused launch saves ~14 us of launch gaps when
+    // launched eagerly; inside a CUDA graph the gaps are gone and the separate
+    // kernels, at full occupancy, are ~6 us faster -> unfused when capturing)
+    int fused_kp = 0, fused_grid = 0;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    if (!gauss && N > 0 && !c->no_fused_bin && cap == cudaStreamCaptureStatusNone) {
+      const int kps[3] = {2, 4, 8};
+      for (int q = 0; q < 3; ++q)
+        if (c->bin_grid[q] > 0 && N <= (int64_t)kps[q] * c->bin_grid[q] * kBinThreads) {
+          fused_kp = kps[q];
+          fused_grid = c->bin_grid[q];
+          break;
+        }
+    }
+    uint32_t* dk = debug ? (uint32_t*)vs.dbg_key.p : nullptr;
+    uint32_t* dt = debug ? (uint32_t*)vs.dbg_tiles.p : nullptr;
+    if (fused_kp) {
+      const uint64_t need = bound;
+      if ((st = ensure(c->entries, (size_t)need * 8, s))) return st;
+      if ((st = ensure(c->tmp, (size_t)need * 8, s))) return st;
+      if ((st = ensure(vs.sorted_idx, (size_t)need * 4, s))) return st;
+      if ((st = ensure(c->agg, (size_t)fused_grid * 4, s))) return st;
+      vs.idx_cap = need;
+      StageTimer tm(c, s, kStBin, 1);
+      PointRec* recp = (PointRec*)vs.rec.p;
+      uint32_t* rg = (uint32_t*)vs.ranges.p;
+      uint32_t* ag = (uint32_t*)c->agg.p;
+      uint32_t* bt = (uint32_t*)c->big_tiles.p;
+      uint32_t* be = (uint32_t*)c->big_elem.p;
+      uint32_t* bc = (uint32_t*)c->big_chunk.p;
+      unsigned long long* en = (unsigned long long*)c->entries.p;
+      unsigned long long* tp = (unsigned long long*)c->tmp.p;
+      uint32_t* si = (uint32_t*)vs.sorted_idx.p;
+      int Ti = T;
+      int64_t Nn = N;
+      bool pk = packed;
+      void* args[] = {(void*)&dc, (void*)&g, (void*)&xyz, (void*)&opacity, (void*)&feat_v, (void*)&pk,
+                      (void*)&Nn, (void*)&Ti, (void*)&recp, (void*)&tc, (void*)&rg, (void*)&ag,
+                      (void*)&bt, (void*)&be, (void*)&bc, (void*)&sc, (void*)&en, (void*)&tp,
+                      (void*)&si, (void*)&dk, (void*)&dt};
+      void* fn = fused_kp == 2 ? (void*)k_bin_bilinear<2> : fused_kp == 4 ? (void*)k_bin_bilinear<4>
+                                                                          : (void*)k_bin_bilinear<8>;
+      CK(cudaLaunchCooperativeKernel(fn, fused_grid, kBinThreads, args, 0, s));
+    }
+    if (N > 0 && !fused_kp) {
       StageTimer tm(c, s, kStProject, 1);
-      uint32_t* dk = debug ? (uint32_t*)vs.dbg_key.p : nullptr;
-      uint32_t* dt = debug ? (uint32_t*)vs.dbg_tiles.p : nullptr;
       if (gauss)
         k_project_count<1><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N,
                                                            (PointRec*)vs.rec.p, tc, nullptr, dk, dt);
@@ -505,7 +566,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
                                                            dk, dt);
       CK(cudaGetLastError());
     }
-    {
+    if (!fused_kp) {
       StageTimer tm(c, s, kStScan, 1);
       k_scan_tiles<<<scan_blocks, kScanThreads, 0, s>>>(T, tc, (uint32_t*)vs.ranges.p,
                                                         (uint32_t*)c->cursor.p,
@@ -521,11 +582,13 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       need = c->host_scalars[0];
       if (need >= 0xFFFFFFFFull) return INPC_KEY_OVERFLOW;
     }
-    if ((st = ensure(c->entries, (size_t)(need ? need : 1) * 8, s))) return st;
-    if ((st = ensure(c->tmp, (size_t)(need ? need : 1) * 8, s))) return st;
-    if ((st = ensure(vs.sorted_idx, (size_t)(need ? need : 1) * 4, s))) return st;
-    vs.idx_cap = need;
-    if (N > 0) {
+    if (!fused_kp) {
+      if ((st = ensure(c->entries, (size_t)(need ? need : 1) * 8, s))) return st;
+      if ((st = ensure(c->tmp, (size_t)(need ? need : 1) * 8, s))) return st;
+      if ((st = ensure(vs.sorted_idx, (size_t)(need ? need : 1) * 4, s))) return st;
+      vs.idx_cap = need;
+    }
+    if (N > 0 && !fused_kp) {
       StageTimer tm(c, s, kStScatter, 1);
       if (gauss)
         k_scatter<1><<<nblk, kPointThreads, 0, s>>>(g, (const PointRec*)vs.rec.p, N, (uint32_t*)c->cursor.p,
@@ -538,7 +601,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
                                                        (unsigned long long*)c->entries.p);
       CK(cudaGetLastError());
     }
-    if (N > kWarpSortCap) {  // a tile can only exceed the SMEM cap with > cap points
+    if (N > kWarpSortCap && !fused_kp) {  // a tile can only exceed the cap with > cap points
       StageTimer tm(c, s, kStSortBig, 1);
       const uint32_t* r = (const uint32_t*)vs.ranges.p;
       const uint32_t* bt = (const uint32_t*)c->big_tiles.p;

@@ -431,17 +431,15 @@ __device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a,
 // the element / chunk prefixes of the big-tile list, (1) chunks of kBigChunk
 // keys are sorted in SMEM, (2) runs are merged pairwise (rank by binary
 // search; keys are unique), (3) the point indices go to sorted_idx.  Grid-
-// synchronised between phases; returns at once if no tile is big.
-__global__ void __launch_bounds__(kBigThreads) k_sort_big(
+// synchronised between phases; returns at once if no tile is big.  Any
+// block size <= kBigThreads; s holds kBigChunk keys.
+__device__ __forceinline__ void big_sort_body(
+    cooperative_groups::grid_group& grid, unsigned long long* s, uint32_t* carry,
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles,
-    uint32_t* big_elem, uint32_t* big_chunk, ViewScalars* sc,
-    unsigned long long* entries, unsigned long long* tmp, uint32_t* __restrict__ sorted_idx) {
-  namespace cg = cooperative_groups;
-  const uint32_t nb = sc->num_big;
+    uint32_t* big_elem, uint32_t* big_chunk, ViewScalars* sc, unsigned long long* entries,
+    unsigned long long* tmp, uint32_t* __restrict__ sorted_idx) {
+  const uint32_t nb = *(volatile uint32_t*)&sc->num_big;
   if (nb == 0) return;
-  cg::grid_group grid = cg::this_grid();
-  __shared__ unsigned long long s[kBigChunk];
-  __shared__ uint32_t carry[2];
   if (blockIdx.x == 0) {
     // exclusive prefixes of sizes and chunk counts (list order is arbitrary;
     // it only decides which CTA works on what)
@@ -457,15 +455,15 @@ __global__ void __launch_bounds__(kBigThreads) k_sort_big(
         ch = (sz + kBigChunk - 1) / kBigChunk;
       }
       tot[threadIdx.x] = sz;
-      tot[kBigThreads + threadIdx.x] = ch;
+      tot[blockDim.x + threadIdx.x] = ch;
       __syncthreads();
-      if (threadIdx.x == 0) {  // serial per 512 tiles: big tiles are few
+      if (threadIdx.x == 0) {  // serial per block of tiles: big tiles are few
         uint32_t a = carry[0], c = carry[1];
         for (uint32_t k = 0; k < blockDim.x && b0 + k < nb; ++k) {
           big_elem[b0 + k] = a;
           big_chunk[b0 + k] = c;
           a += tot[k];
-          c += tot[kBigThreads + k];
+          c += tot[blockDim.x + k];
         }
         carry[0] = a;
         carry[1] = c;
@@ -528,6 +526,167 @@ __global__ void __launch_bounds__(kBigThreads) k_sort_big(
     sc->num_big = 0u;
     sc->max_big = 0u;
   }
+}
+
+__global__ void __launch_bounds__(kBigThreads) k_sort_big(
+    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles,
+    uint32_t* big_elem, uint32_t* big_chunk, ViewScalars* sc,
+    unsigned long long* entries, unsigned long long* tmp, uint32_t* __restrict__ sorted_idx) {
+  __shared__ unsigned long long s[kBigChunk];
+  __shared__ uint32_t carry[2];
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  big_sort_body(grid, s, carry, ranges, big_tiles, big_elem, big_chunk, sc, entries, tmp, sorted_idx);
+}
+
+// ---------------------------------------------------------------- H1..H6 fused (bilinear)
+// One cooperative launch for the whole binning of a bilinear view: every
+// thread keeps KP points' depth key, tile block and entry slots in
+// registers across the grid barriers, so the slots never go to memory and
+// the records are not read back.
+//   phase 1  H1+H2: project, record, atomic slot per (point, tile)
+//   phase 2  H3:    scan of the tile counts (per-CTA block scan + prefix of
+//                   the CTA aggregates), counts zeroed for the next call
+//   phase 3  H5:    scatter of the 64-bit keys to ranges[tile] + slot
+//   phase 4  H4/H6: tiles over the warp-sort cap (big_sort_body)
+constexpr int kBinThreads = 512;
+
+template <int KP>
+__global__ void __launch_bounds__(kBinThreads) k_bin_bilinear(
+    DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ opacity,
+    const float* __restrict__ feat, bool pack, int64_t N, int T, PointRec* __restrict__ rec,
+    uint32_t* counts, uint32_t* ranges, uint32_t* agg, uint32_t* big_tiles, uint32_t* big_elem,
+    uint32_t* big_chunk, ViewScalars* sc, unsigned long long* entries, unsigned long long* tmp,
+    uint32_t* sorted_idx, uint32_t* __restrict__ dbg_key, uint32_t* __restrict__ dbg_tiles) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned long long s[kBigChunk];
+  __shared__ uint32_t carry[2];
+  __shared__ uint32_t wt[kBinThreads / 32];
+  const int64_t nthr = (int64_t)gridDim.x * kBinThreads;
+  const int64_t tid = (int64_t)blockIdx.x * kBinThreads + threadIdx.x;
+  // ---- phase 1
+  uint32_t key[KP], tb[KP], sl[KP][4], vm[KP];
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    const int64_t i = tid + k * nthr;
+    key[k] = 0u;
+    vm[k] = 0u;
+    if (i >= N) continue;
+    Proj p;
+    Foot f;
+    const bool vis = project_point(cam, __ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2), p);
+    const bool ok = vis && foot_bilinear(g, p.u, p.v, f);
+    PointRec pr;
+    pr.a = make_float4(p.u, p.v, ok ? p.zc : 0.0f, __ldg(opacity + i));
+    pr.b = pack ? __ldg(reinterpret_cast<const float4*>(feat) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    rec[i] = pr;
+    if (dbg_key) {
+      dbg_key[i] = vis ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
+      dbg_tiles[i] = ok ? (uint32_t)((f.xhi / kTile - f.xlo / kTile + 1) * (f.yhi / kTile - f.ylo / kTile + 1)) : 0u;
+    }
+    if (!ok) continue;
+    const int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
+    const int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
+    key[k] = __float_as_uint(p.zc);
+    tb[k] = (uint32_t)(ty_lo * g.tiles_x + tx_lo);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int tx = tx_lo + (c & 1), ty = ty_lo + (c >> 1);
+      if (tx <= tx_hi && ty <= ty_hi) {
+        sl[k][c] = atomicAdd(counts + (size_t)ty * g.tiles_x + tx, 1u);
+        vm[k] |= 1u << c;
+      }
+    }
+  }
+  grid.sync();
+  // ---- phase 2: CTA b scans tiles [b*per, (b+1)*per)
+  const int per = (T + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per, t1 = min(T, t0 + per);
+  const int items = (per + kBinThreads - 1) / kBinThreads;  // consecutive tiles per thread
+  const int my0 = t0 + threadIdx.x * items;
+  uint32_t sum = 0;
+  for (int q = 0; q < items; ++q) {
+    const int t = my0 + q;
+    if (t < t1) sum += counts[t];
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wt[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = lane < kBinThreads / 32 ? wt[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < kBinThreads / 32) wt[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t excl = (wid ? wt[wid - 1] : 0u) + x - sum;
+  if (threadIdx.x == 0) agg[blockIdx.x] = wt[kBinThreads / 32 - 1];
+  grid.sync();
+  // prefix of the preceding CTAs' aggregates
+  uint32_t pre = 0;
+  for (int b = threadIdx.x; b < (int)blockIdx.x; b += kBinThreads) pre += agg[b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  __syncthreads();
+  if (lane == 0) wt[wid] = pre;
+  __syncthreads();
+  uint32_t cta_pre = 0;
+#pragma unroll
+  for (int w = 0; w < kBinThreads / 32; ++w) cta_pre += wt[w];
+  uint32_t off = cta_pre + excl, mx = 0;
+  for (int q = 0; q < items; ++q) {
+    const int t = my0 + q;
+    if (t >= t1) break;
+    const uint32_t c = counts[t];
+    counts[t] = 0u;  // ready for the next call
+    ranges[t] = off;
+    if (c > (uint32_t)kWarpSortCap) {
+      big_tiles[atomicAdd(&sc->num_big, 1u)] = t;
+      mx = max(mx, c);
+    }
+    off += c;
+  }
+  if (mx) atomicMax(&sc->max_big, mx);
+  grid.sync();
+  if (blockIdx.x == 0) {  // grand total = F_t
+    uint32_t tot = 0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kBinThreads) tot += agg[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0) wt[wid] = tot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int w = 0; w < kBinThreads / 32; ++w) t += wt[w];
+      ranges[T] = t;
+      sc->Ft = t;
+    }
+  }
+  // ---- phase 3: scatter
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    if (!key[k]) continue;
+    const int64_t i = tid + k * nthr;
+    const unsigned long long kv = ((unsigned long long)key[k] << 32) | (uint32_t)i;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (vm[k] & (1u << c)) {
+        const uint32_t t = tb[k] + (uint32_t)(c & 1) + (uint32_t)(c >> 1) * g.tiles_x;
+        entries[ranges[t] + sl[k][c]] = kv;
+      }
+  }
+  grid.sync();
+  // ---- phase 4: big tiles
+  big_sort_body(grid, s, carry, ranges, big_tiles, big_elem, big_chunk, sc, entries, tmp, sorted_idx);
 }
 
 // ---------------------------------------------------------------- H7 / H8 per-warp staging

@@ -262,3 +262,29 @@ def test_cfg4_global_cloud_sampled(inpc, ctx):
         ty, tx = divmod(int(t), 240)
         mask[ty * 8:(ty + 1) * 8, tx * 8:(tx + 1) * 8] = True
     check_image(c, res, "bilinear", pixel_mask=mask)
+
+
+# ------------------------------------------------------------------ both binning paths
+@pytest.fixture(scope="module")
+def ctx_unfused(inpc):
+    """A context that bins with the separate project / scan / scatter /
+    big-sort kernels instead of the fused cooperative one."""
+    import os
+    os.environ["INPC_NO_FUSED_BIN"] = "1"
+    try:
+        return inpc.Context(0)
+    finally:
+        del os.environ["INPC_NO_FUSED_BIN"]
+
+
+@pytest.mark.parametrize("seed", [1, 101])
+def test_unfused_binning_cfg1(inpc, ctx_unfused, seed):
+    run_full(inpc, ctx_unfused, synthgen.config1(seed=seed))
+
+
+def test_unfused_binning_cfg2(inpc, ctx_unfused):
+    run_full(inpc, ctx_unfused, synthgen.config2())
+
+
+def test_unfused_big_tile(inpc, ctx_unfused):
+    test_one_hot_tile_over_smem_cap(inpc, ctx_unfused, 5000)
