@@ -68,6 +68,20 @@ extern "C" {
 #define INPC_FLAG_SKIP_ZERO_ALPHA_GRAD (1u << 1) /* R13: original INPC behaviour (A/B) */
 #define INPC_FLAG_DEBUG (1u << 2)                /* keep per-point depth keys / tile
                                                     counts for inpc_debug_export      */
+#define INPC_FLAG_SH_FEATURES (1u << 3)          /* NEXT f1: `feat` holds real SH
+                                                    coefficients of degree <= 2, [N,C,9]
+                                                    ([V,N,C,9] with feat_view_stride =
+                                                    N*C*9); features f_c = sum_k
+                                                    coeff[c][k] Y_k(d), d = unit vector
+                                                    from the camera centre to the point
+                                                    (R26); the backward accumulates
+                                                    dL/dcoeff into g_point_feat [N,C,9] */
+#define INPC_FLAG_ENV_BACKGROUND (1u << 4)       /* NEXT f2: `bg` is an
+                                                    equirectangular map [env_h,env_w,C]
+                                                    (bg_view_stride 0 or env_h*env_w*C);
+                                                    each pixel's background is its
+                                                    bilinear lookup along the pixel's
+                                                    world ray (R27); not differentiated */
 
 /* Pinhole camera (R2): x_cam = R x_world + t, R row-major 3x3;
  * u = fx x_cam/z_cam + cx, v = fy y_cam/z_cam + cy; pixel (i, j) has its
@@ -91,6 +105,7 @@ typedef struct {
   int32_t tile_y_begin; /* screen band [begin, end) in 8-pixel tile rows for        */
   int32_t tile_y_end;   /*   sort-first sharding; 0, 0 = whole image                */
   uint32_t flags;       /* INPC_FLAG_*                                              */
+  int32_t env_h, env_w; /* environment map size with INPC_FLAG_ENV_BACKGROUND, else 0 */
 } inpc_raster_cfg;
 
 typedef struct inpc_ctx inpc_ctx;

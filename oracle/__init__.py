@@ -83,6 +83,9 @@ def _load():
             lib.or_fragments.argtypes = [P, P, i64, P, P, P, P, P, P, i64]
             lib.or_fragments.restype = i64
             lib.or_max_threads.restype = ct.c_int
+            lib.or_sh_basis.argtypes = [P, P]
+            lib.or_sh_features.argtypes = [P, i64, ct.c_int, P, P, P, P]
+            lib.or_env_background.argtypes = [P, ct.c_int, ct.c_int, ct.c_int, P, ct.c_int, ct.c_int, P]
             _lib = lib
     return _lib
 
@@ -238,3 +241,35 @@ def fragments(cam, xyz, H, W, mode="bilinear", **kw):
     lib.or_fragments(ct.byref(c), ct.byref(g), N, _p(xyz), _p(out["pix"]), _p(out["idx"]),
                      _p(out["key"]), _p(out["w32"]), _p(out["w64"]), n)
     return {k: v[:n] for k, v in out.items()}
+
+
+def sh_basis(d):
+    """Real SH basis of degree <= 2 (9 values) at unit direction d (fp64)."""
+    d = np.ascontiguousarray(d, np.float64).reshape(3)
+    Y = np.zeros(9)
+    _load().or_sh_basis(_p(d), _p(Y))
+    return Y
+
+
+def sh_features(cam, xyz, sh):
+    """Features [N, C] from SH coefficients [N, C, 9] at the view directions of
+    camera `cam`; also returns the basis values [N, 9]."""
+    xyz = _f32(xyz, (-1, 3))
+    N = xyz.shape[0]
+    sh = _f64(sh, (N, -1, 9))
+    C = sh.shape[1]
+    feat = np.zeros((N, C)); Y = np.zeros((N, 9))
+    c = _cam(cam)
+    _load().or_sh_features(ct.byref(c), N, C, _p(xyz), _p(sh), _p(feat), _p(Y))
+    return feat, Y
+
+
+def env_background(cam, env, H, W):
+    """Per-pixel background [H, W, C] from an equirectangular map [He, We, C]
+    (P:185-192)."""
+    env = _f32(env)
+    He, We, C = env.shape
+    bg = np.zeros((H, W, C))
+    c = _cam(cam)
+    _load().or_env_background(ct.byref(c), int(H), int(W), int(C), _p(env), int(He), int(We), _p(bg))
+    return bg

@@ -546,3 +546,89 @@ int64_t or_fragments(const or_camera* c, const or_cfg* g, int64_t N, const float
   free(fr.a);
   return n;
 }
+
+/* ---- NEXT f1: degree-2 spherical-harmonics features -------------
+ * f_c = sum_k coeff[c][k] Y_k(d), d = unit vector from the camera centre to
+ * the point, real SH basis with the standard constants (SPEC S:~455 design
+ * decision; R26).  fp64. */
+static const double OR_SH_C0 = 0.28209479177387814;
+static const double OR_SH_C1 = 0.4886025119029199;
+static const double OR_SH_C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                                   -1.0925484305920792, 0.5462742152960396};
+
+void or_sh_basis(const double* d, double* Y) {
+  double x = d[0], y = d[1], z = d[2];
+  Y[0] = OR_SH_C0;
+  Y[1] = -OR_SH_C1 * y;
+  Y[2] = OR_SH_C1 * z;
+  Y[3] = -OR_SH_C1 * x;
+  Y[4] = OR_SH_C2[0] * x * y;
+  Y[5] = OR_SH_C2[1] * y * z;
+  Y[6] = OR_SH_C2[2] * (2.0 * z * z - x * x - y * y);
+  Y[7] = OR_SH_C2[3] * x * z;
+  Y[8] = OR_SH_C2[4] * (x * x - y * y);
+}
+
+/* camera centre in world space: x_cam = R x + t = 0  ->  c = -R^T t */
+static void cam_centre(const or_camera* c, double* ctr) {
+  for (int k = 0; k < 3; k++)
+    ctr[k] = -((double)c->R[0 * 3 + k] * c->t[0] + (double)c->R[1 * 3 + k] * c->t[1] +
+               (double)c->R[2 * 3 + k] * c->t[2]);
+}
+
+/* feat [N, C] (fp64) from sh [N, C, 9]; Ybuf [N, 9] optional (the basis per point) */
+void or_sh_features(const or_camera* c, int64_t N, int C, const float* xyz, const double* sh,
+                    double* feat, double* Ybuf) {
+  double ctr[3];
+  cam_centre(c, ctr);
+  for (int64_t i = 0; i < N; i++) {
+    double d[3] = {xyz[3 * i] - ctr[0], xyz[3 * i + 1] - ctr[1], xyz[3 * i + 2] - ctr[2]};
+    double n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    if (n > 0) { d[0] /= n; d[1] /= n; d[2] /= n; }
+    double Y[9];
+    or_sh_basis(d, Y);
+    for (int ch = 0; ch < C; ch++) {
+      double s = 0;
+      for (int k = 0; k < 9; k++) s += sh[(i * C + ch) * 9 + k] * Y[k];
+      feat[i * C + ch] = s;
+    }
+    if (Ybuf) for (int k = 0; k < 9; k++) Ybuf[i * 9 + k] = Y[k];
+  }
+}
+
+/* ---- NEXT f2: equirectangular environment-map background ---
+ * Pixel ray through the pixel centre, rotated to world space; u =
+ * (atan2(dx, dz) / 2 pi + 1/2) We, v = acos(dy) / pi He; texel (i, j) centre
+ * at (i + 1/2, j + 1/2); bilinear with azimuthal wrap and polar clamp
+ * (R27).  bg [H, W, C] fp64 from env [He, We, C]. */
+void or_env_background(const or_camera* c, int H, int W, int C, const float* env, int He, int We,
+                       double* bg) {
+  const double PI = 3.14159265358979323846;
+  for (int py = 0; py < H; py++)
+    for (int px = 0; px < W; px++) {
+      double dc[3] = {((px + 0.5) - c->cx) / c->fx, ((py + 0.5) - c->cy) / c->fy, 1.0};
+      double n = sqrt(dc[0] * dc[0] + dc[1] * dc[1] + dc[2] * dc[2]);
+      double d[3];
+      for (int k = 0; k < 3; k++)   /* world = R^T cam */
+        d[k] = (c->R[0 * 3 + k] * dc[0] + c->R[1 * 3 + k] * dc[1] + c->R[2 * 3 + k] * dc[2]) / n;
+      double u = (atan2(d[0], d[2]) / (2 * PI) + 0.5) * We;
+      double dy = d[1] < -1 ? -1 : (d[1] > 1 ? 1 : d[1]);
+      double v = acos(dy) / PI * He;
+      double x = u - 0.5, y = v - 0.5;
+      double fx0 = floor(x), fy0 = floor(y);
+      double a = x - fx0, b = y - fy0;
+      long i0 = (long)fx0, j0 = (long)fy0;
+      long i1 = i0 + 1, j1 = j0 + 1;
+      i0 = ((i0 % We) + We) % We; i1 = ((i1 % We) + We) % We;
+      if (j0 < 0) j0 = 0;
+      if (j0 > He - 1) j0 = He - 1;
+      if (j1 < 0) j1 = 0;
+      if (j1 > He - 1) j1 = He - 1;
+      for (int ch = 0; ch < C; ch++) {
+        double t00 = env[((size_t)j0 * We + i0) * C + ch], t10 = env[((size_t)j0 * We + i1) * C + ch];
+        double t01 = env[((size_t)j1 * We + i0) * C + ch], t11 = env[((size_t)j1 * We + i1) * C + ch];
+        bg[((size_t)py * W + px) * C + ch] =
+            (1 - a) * (1 - b) * t00 + a * (1 - b) * t10 + (1 - a) * b * t01 + a * b * t11;
+      }
+    }
+}

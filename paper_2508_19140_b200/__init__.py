@@ -26,6 +26,8 @@ SPLAT_BILINEAR, SPLAT_GAUSSIAN = 0, 1
 FLAG_SIGMA_IS_PIXELS = 1 << 0
 FLAG_SKIP_ZERO_ALPHA_GRAD = 1 << 1
 FLAG_DEBUG = 1 << 2
+FLAG_SH_FEATURES = 1 << 3
+FLAG_ENV_BACKGROUND = 1 << 4
 TILE = 8
 
 EXPORTS = ("inpc_ctx_create", "inpc_ctx_destroy", "inpc_rasterize_fwd", "inpc_rasterize_bwd",
@@ -51,7 +53,8 @@ class RasterCfg(ct.Structure):
     _fields_ = [("H", ct.c_int32), ("W", ct.c_int32), ("C", ct.c_int32),
                 ("splat_mode", ct.c_int32), ("sigma", ct.c_float), ("dilation", ct.c_float),
                 ("alpha_max", ct.c_float), ("t_min", ct.c_float), ("tile_y_begin", ct.c_int32),
-                ("tile_y_end", ct.c_int32), ("flags", ct.c_uint32)]
+                ("tile_y_end", ct.c_int32), ("flags", ct.c_uint32), ("env_h", ct.c_int32),
+                ("env_w", ct.c_int32)]
 
 
 def _load():
@@ -107,7 +110,7 @@ def make_camera(cam) -> Camera:
 
 
 def make_cfg(H, W, C, mode="bilinear", sigma=0.0, dilation=0.16, alpha_max=0.99, t_min=1e-4,
-             band=None, flags=0) -> RasterCfg:
+             band=None, flags=0, env_hw=None) -> RasterCfg:
     g = RasterCfg()
     g.H, g.W, g.C = int(H), int(W), int(C)
     g.splat_mode = {"bilinear": SPLAT_BILINEAR, "gaussian": SPLAT_GAUSSIAN,
@@ -116,6 +119,9 @@ def make_cfg(H, W, C, mode="bilinear", sigma=0.0, dilation=0.16, alpha_max=0.99,
     g.alpha_max, g.t_min = float(alpha_max), float(t_min)
     g.tile_y_begin, g.tile_y_end = (0, 0) if band is None else (int(band[0]), int(band[1]))
     g.flags = int(flags)
+    if env_hw is not None:
+        g.env_h, g.env_w = int(env_hw[0]), int(env_hw[1])
+        g.flags |= FLAG_ENV_BACKGROUND
     return g
 
 
@@ -138,6 +144,18 @@ def _cams(cams):
         cams = [cams]
     arr = (Camera * len(cams))(*[make_camera(c) for c in cams])
     return arr, len(cams)
+
+
+def _strides(cfg, N, feat, bg):
+    """Per-view strides of feat ([N,C] / [V,N,C], or SH [N,C,9] / [V,N,C,9])
+    and bg ([H,W,C] / [V,H,W,C], or env map [He,We,C] / [V,He,We,C])."""
+    sh = bool(cfg.flags & FLAG_SH_FEATURES)
+    per_feat = N * cfg.C * (9 if sh else 1)
+    fstride = per_feat if feat.dim() == (4 if sh else 3) else 0
+    bstride = 0
+    if bg is not None and bg.dim() == 4:
+        bstride = bg[0].numel()
+    return fstride, bstride
 
 
 class Context:
@@ -172,8 +190,7 @@ class Context:
         cam_arr, V = _cams(cams)
         N = xyz.shape[0]
         C, H, W = cfg.C, cfg.H, cfg.W
-        fstride = 0 if feat.dim() == 2 else N * C
-        bstride = 0 if bg is None or bg.dim() == 3 else H * W * C
+        fstride, bstride = _strides(cfg, N, feat, bg)
         dev = xyz.device
         if out is None:
             out = dict(F=torch.empty((V, H, W, C), device=dev, dtype=torch.float32),
@@ -197,8 +214,7 @@ class Context:
         cam_arr, V = _cams(cams)
         N = xyz.shape[0]
         C, H, W = cfg.C, cfg.H, cfg.W
-        fstride = 0 if feat.dim() == 2 else N * C
-        bstride = 0 if bg is None or bg.dim() == 3 else H * W * C
+        fstride, bstride = _strides(cfg, N, feat, bg)
         if g_feat is None:
             g_feat = torch.zeros_like(feat)
         if g_opacity is None:

@@ -34,13 +34,15 @@ enum Stage : int {
   kStBlendFwd,
   kStBlendBwd,
   kStBin,
+  kStShGrad,
   kNumStages
 };
-const char* kStageNames[kNumStages] = {"memset", "project_count", "scan_tiles", "scatter",
-                                       "sort_big", "blend_fwd", "blend_bwd", "bin_fused"};
+const char* kStageNames[kNumStages] = {"memset",    "project_count", "scan_tiles", "scatter",
+                                       "sort_big",  "blend_fwd",     "blend_bwd",  "bin_fused",
+                                       "sh_grad"};
 
 struct ViewState {
-  Buf ranges, sorted_idx, T_final, last, dbg_key, dbg_tiles, scalars, rec;
+  Buf ranges, sorted_idx, T_final, last, dbg_key, dbg_tiles, scalars, rec, feat_eval;
   uint64_t idx_cap = 0;
 };
 
@@ -56,7 +58,7 @@ struct inpc_ctx {
   int num_sms = 148;
   int big_grid = 0;
   // scratch (shared by views, stream ordered)
-  Buf zeroed, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg;
+  Buf zeroed, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg, g_eval;
   int bin_grid[3] = {0, 0, 0};  // cooperative grid of k_bin_bilinear<2,4,8>
   bool no_fused_bin = false;     // env INPC_NO_FUSED_BIN=1: separate binning kernels
   uint64_t entry_cap = 0;
@@ -187,6 +189,8 @@ int validate_cfg(const inpc_raster_cfg* cfg, const inpc_camera* cams, int32_t V)
     if (!(cfg->dilation >= 0.0f) || !isfinite(cfg->dilation)) return INPC_INVALID_ARG;
     if ((cfg->flags & INPC_FLAG_SIGMA_IS_PIXELS) && !(cfg->sigma > 0.0f)) return INPC_INVALID_ARG;
   }
+  if ((cfg->flags & INPC_FLAG_ENV_BACKGROUND) && (cfg->env_h <= 0 || cfg->env_w <= 0))
+    return INPC_INVALID_ARG;
   int tiles_y = (cfg->H + kTile - 1) / kTile;
   if (!(cfg->tile_y_begin == 0 && cfg->tile_y_end == 0)) {
     if (cfg->tile_y_begin < 0 || cfg->tile_y_end > tiles_y || cfg->tile_y_begin >= cfg->tile_y_end)
@@ -209,6 +213,9 @@ void make_dev(const inpc_raster_cfg* cfg, const inpc_camera& cam, DevCam& dc, De
   dc.cx = cam.cx;
   dc.cy = cam.cy;
   dc.z_near = cam.z_near;
+  for (int k = 0; k < 3; ++k)  // camera centre -R^T t
+    dc.cw[k] = (float)-((double)cam.R[k] * cam.t[0] + (double)cam.R[3 + k] * cam.t[1] +
+                        (double)cam.R[6 + k] * cam.t[2]);
   g.H = cfg->H;
   g.W = cfg->W;
   g.C = cfg->C;
@@ -225,6 +232,10 @@ void make_dev(const inpc_raster_cfg* cfg, const inpc_camera& cam, DevCam& dc, De
   g.flags = 0;
   if (cfg->flags & INPC_FLAG_SIGMA_IS_PIXELS) g.flags |= kFlagSigmaPx;
   if (cfg->flags & INPC_FLAG_SKIP_ZERO_ALPHA_GRAD) g.flags |= kFlagSkipZero;
+  if (cfg->flags & INPC_FLAG_SH_FEATURES) g.flags |= kFlagSH;
+  if (cfg->flags & INPC_FLAG_ENV_BACKGROUND) g.flags |= kFlagEnv;
+  g.env_h = cfg->env_h;
+  g.env_w = cfg->env_w;
 }
 
 int cmax_for(int C) { return C <= 4 ? 4 : C <= 8 ? 8 : C <= 16 ? 16 : C <= 32 ? 32 : 64; }
@@ -364,12 +375,12 @@ int inpc_ctx_destroy(inpc_ctx* c) {
   if (!c) return INPC_INVALID_ARG;
   DeviceGuard dg(c->device);
   cudaDeviceSynchronize();
-  for (Buf* b : {&c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots, &c->agg,
+  for (Buf* b : {&c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots, &c->agg, &c->g_eval,
                  &c->tmp, &c->overflow})
     free_buf(*b);
   for (auto& v : c->views)
     for (Buf* b : {&v.ranges, &v.sorted_idx, &v.T_final, &v.last, &v.dbg_key, &v.dbg_tiles, &v.scalars,
-                   &v.rec})
+                   &v.rec, &v.feat_eval})
       free_buf(*b);
   for (auto& e : c->pending) {
     cudaEventDestroy(e.a);
@@ -442,9 +453,13 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   int st = validate_cfg(cfg, cams, V);
   if (st) return st;
   if (N < 0 || N > 0xFFFFFFFFll) return N < 0 ? INPC_INVALID_ARG : INPC_KEY_OVERFLOW;
-  if (feat_view_stride != 0 && feat_view_stride != N * cfg->C) return INPC_INVALID_ARG;
+  const bool sh = (cfg->flags & INPC_FLAG_SH_FEATURES) != 0;
+  const bool env = (cfg->flags & INPC_FLAG_ENV_BACKGROUND) != 0;
+  if (feat_view_stride != 0 && feat_view_stride != N * cfg->C * (sh ? 9 : 1)) return INPC_INVALID_ARG;
   const int64_t P = (int64_t)cfg->H * cfg->W;
-  if (bg_view_stride != 0 && bg_view_stride != P * cfg->C) return INPC_INVALID_ARG;
+  const int64_t bg_per_view = env ? (int64_t)cfg->env_h * cfg->env_w * cfg->C : P * cfg->C;
+  if (bg_view_stride != 0 && bg_view_stride != bg_per_view) return INPC_INVALID_ARG;
+  if (env && !bg) return INPC_INVALID_ARG;
   DeviceGuard dg(c->device);
   if (N > 0 && (!is_device_ptr(xyz) || !is_device_ptr(feat) || !is_device_ptr(opacity)))
     return INPC_INVALID_ARG;
@@ -504,6 +519,12 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     }
     const float* feat_v = feat + (size_t)v * feat_view_stride;
     const float* bg_v = bg ? bg + (size_t)v * bg_view_stride : nullptr;
+    float* feat_out = nullptr;  // SH features evaluated for this view (when not packed)
+    if (sh && !packed && N > 0) {
+      if ((st = ensure(vs.feat_eval, (size_t)N * cfg->C * 4, s))) return st;
+      feat_out = (float*)vs.feat_eval.p;
+    }
+    const float* feat_blend = feat_out ? feat_out : feat_v;
     uint32_t* tc = (uint32_t*)c->zeroed.p;
     unsigned long long* scan_state = (unsigned long long*)((char*)c->zeroed.p + count_bytes);
     ScanCtl* scan_ctl = (ScanCtl*)(scan_state + scan_blocks);
@@ -550,7 +571,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       void* args[] = {(void*)&dc, (void*)&g, (void*)&xyz, (void*)&opacity, (void*)&feat_v, (void*)&pk,
                       (void*)&Nn, (void*)&Ti, (void*)&recp, (void*)&tc, (void*)&rg, (void*)&ag,
                       (void*)&bt, (void*)&be, (void*)&bc, (void*)&sc, (void*)&en, (void*)&tp,
-                      (void*)&si, (void*)&dk, (void*)&dt};
+                      (void*)&si, (void*)&dk, (void*)&dt, (void*)&feat_out};
       void* fn = fused_kp == 2 ? (void*)k_bin_bilinear<2> : fused_kp == 4 ? (void*)k_bin_bilinear<4>
                                                                           : (void*)k_bin_bilinear<8>;
       CK(cudaLaunchCooperativeKernel(fn, fused_grid, kBinThreads, args, 0, s));
@@ -559,11 +580,12 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       StageTimer tm(c, s, kStProject, 1);
       if (gauss)
         k_project_count<1><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N,
-                                                           (PointRec*)vs.rec.p, tc, nullptr, dk, dt);
+                                                           (PointRec*)vs.rec.p, tc, nullptr, dk, dt,
+                                                           feat_out);
       else
         k_project_count<0><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N,
                                                            (PointRec*)vs.rec.p, tc, (uint4*)c->slots.p,
-                                                           dk, dt);
+                                                           dk, dt, feat_out);
       CK(cudaGetLastError());
     }
     if (!fused_kp) {
@@ -625,11 +647,11 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       o.T_final = (float*)vs.T_final.p;
       o.last = (uint32_t*)vs.last.p;
       if (gauss)
-        dispatch_blend_fwd<1>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, false, bg_v,
+        dispatch_blend_fwd<1>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_blend, false, bg_v,
                               (const uint32_t*)vs.ranges.p, (const unsigned long long*)c->entries.p,
                               (uint32_t*)vs.sorted_idx.p, o);
       else
-        dispatch_blend_fwd<0>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, packed, bg_v,
+        dispatch_blend_fwd<0>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_blend, packed, bg_v,
                               (const uint32_t*)vs.ranges.p, (const unsigned long long*)c->entries.p,
                               (uint32_t*)vs.sorted_idx.p, o);
       CK(cudaGetLastError());
@@ -661,9 +683,13 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   int st = validate_cfg(cfg, cams, V);
   if (st) return st;
   if (N < 0) return INPC_INVALID_ARG;
-  if (feat_view_stride != 0 && feat_view_stride != N * cfg->C) return INPC_INVALID_ARG;
+  const bool sh = (cfg->flags & INPC_FLAG_SH_FEATURES) != 0;
+  const bool env = (cfg->flags & INPC_FLAG_ENV_BACKGROUND) != 0;
+  if (feat_view_stride != 0 && feat_view_stride != N * cfg->C * (sh ? 9 : 1)) return INPC_INVALID_ARG;
   const int64_t P = (int64_t)cfg->H * cfg->W;
-  if (bg_view_stride != 0 && bg_view_stride != P * cfg->C) return INPC_INVALID_ARG;
+  const int64_t bg_per_view = env ? (int64_t)cfg->env_h * cfg->env_w * cfg->C : P * cfg->C;
+  if (bg_view_stride != 0 && bg_view_stride != bg_per_view) return INPC_INVALID_ARG;
+  if (env && !bg) return INPC_INVALID_ARG;
   DeviceGuard dg(c->device);
   DevCam dc;
   DevCfg g;
@@ -703,14 +729,29 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     in.g_op = g_opacity;
     const float* feat_v = feat + (size_t)v * feat_view_stride;
     const float* bg_v = bg ? bg + (size_t)v * bg_view_stride : nullptr;
-    StageTimer tm(c, s, kStBlendBwd, 1);
-    if (gauss)
-      dispatch_blend_bwd<1>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, false, bg_v,
-                            (const uint32_t*)vs.ranges.p, (const uint32_t*)vs.sorted_idx.p, in);
-    else
-      dispatch_blend_bwd<0>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, packed, bg_v,
-                            (const uint32_t*)vs.ranges.p, (const uint32_t*)vs.sorted_idx.p, in);
-    CK(cudaGetLastError());
+    if (sh) {
+      // dL/df of this view into a scratch [N, C], then to the SH coefficients
+      if ((st = ensure(c->g_eval, (size_t)N * cfg->C * 4, s))) return st;
+      CK(cudaMemsetAsync(c->g_eval.p, 0, (size_t)N * cfg->C * 4, s));
+      in.g_feat = (float*)c->g_eval.p;
+      if (!packed) feat_v = (const float*)vs.feat_eval.p;
+    }
+    {
+      StageTimer tm(c, s, kStBlendBwd, 1);
+      if (gauss)
+        dispatch_blend_bwd<1>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, false, bg_v,
+                              (const uint32_t*)vs.ranges.p, (const uint32_t*)vs.sorted_idx.p, in);
+      else
+        dispatch_blend_bwd<0>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, packed, bg_v,
+                              (const uint32_t*)vs.ranges.p, (const uint32_t*)vs.sorted_idx.p, in);
+      CK(cudaGetLastError());
+    }
+    if (sh) {
+      StageTimer tm(c, s, kStShGrad, 1);
+      k_sh_grad<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(dc, g, xyz, N, (const float*)c->g_eval.p,
+                                                            g_point_feat + (size_t)v * feat_view_stride);
+      CK(cudaGetLastError());
+    }
   }
   return INPC_OK;
 }

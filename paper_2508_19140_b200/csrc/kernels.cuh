@@ -47,6 +47,40 @@ struct __align__(16) PointRec {
   float4 b;  // features | conic + radius
 };
 
+// NEXT f1: evaluate the point's SH features (feat = coefficients [N, C, 9])
+// into the packed record (C == 4) or the per-view feature buffer feat_out.
+__device__ __forceinline__ void sh_point_features(const DevCam& cam, const DevCfg& g,
+                                                  const float* __restrict__ sh, int64_t i, float X,
+                                                  float Y, float Z, bool packed, float4& F,
+                                                  float* __restrict__ feat_out) {
+  float B[9];
+  sh_dir_basis(cam, X, Y, Z, B);
+  const float* shi = sh + (size_t)i * g.C * 9;
+  if (packed) {
+    F = make_float4(sh_feature(shi, 0, B), sh_feature(shi, 1, B), sh_feature(shi, 2, B),
+                    sh_feature(shi, 3, B));
+  } else {
+    for (int c = 0; c < g.C; ++c) feat_out[(size_t)i * g.C + c] = sh_feature(shi, c, B);
+  }
+}
+
+// NEXT f1 backward: dL/dcoeff[c][k] += dL/df_c Y_k(d)  (g_sh [N, C, 9]).
+__global__ void __launch_bounds__(256) k_sh_grad(DevCam cam, DevCfg g, const float* __restrict__ xyz,
+                                                 int64_t N, const float* __restrict__ g_f,
+                                                 float* __restrict__ g_sh) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  float B[9];
+  sh_dir_basis(cam, __ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2), B);
+  for (int c = 0; c < g.C; ++c) {
+    const float gf = __ldg(g_f + (size_t)i * g.C + c);
+    if (gf == 0.0f) continue;
+    float* o = g_sh + ((size_t)i * g.C + c) * 9;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) o[k] += gf * B[k];
+  }
+}
+
 // kPPT points per thread, loads of all of them issued before any compute so
 // enough bytes are in flight to cover HBM latency.
 template <int MODE>
@@ -54,7 +88,7 @@ __global__ void __launch_bounds__(kPointThreads) k_project_count(
     DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ opacity,
     const float* __restrict__ feat, bool pack, int64_t N, PointRec* __restrict__ rec,
     uint32_t* __restrict__ tile_count, uint4* __restrict__ slots, uint32_t* __restrict__ dbg_key,
-    uint32_t* __restrict__ dbg_tiles) {
+    uint32_t* __restrict__ dbg_tiles, float* __restrict__ feat_out) {
   const int64_t stride = (int64_t)gridDim.x * kPointThreads;
   const int64_t i0 = (int64_t)blockIdx.x * kPointThreads + threadIdx.x;
   float X[kPPT], Y[kPPT], Z[kPPT], O[kPPT];
@@ -67,7 +101,7 @@ __global__ void __launch_bounds__(kPointThreads) k_project_count(
       Y[k] = __ldg(xyz + 3 * i + 1);
       Z[k] = __ldg(xyz + 3 * i + 2);
       O[k] = __ldg(opacity + i);
-      if (MODE == 0 && pack) Fv[k] = __ldg(reinterpret_cast<const float4*>(feat) + i);
+      if (MODE == 0 && pack && !(g.flags & kFlagSH)) Fv[k] = __ldg(reinterpret_cast<const float4*>(feat) + i);
     }
   }
 #pragma unroll
@@ -83,6 +117,8 @@ __global__ void __launch_bounds__(kPointThreads) k_project_count(
       if (MODE == 0) ok = foot_bilinear(g, p.u, p.v, f);
       else ok = gauss_conic(cam, g, p, ca, cb, cc, r) && gauss_rect(g, p.u, p.v, r, f);
     }
+    if ((g.flags & kFlagSH) && ok) sh_point_features(cam, g, feat, i, X[k], Y[k], Z[k], MODE == 0 && pack,
+                                                     Fv[k], feat_out);
     PointRec pr;
     pr.a = make_float4(p.u, p.v, ok ? p.zc : 0.0f, O[k]);
     if (MODE == 0) pr.b = pack ? Fv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -556,7 +592,8 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_bilinear(
     const float* __restrict__ feat, bool pack, int64_t N, int T, PointRec* __restrict__ rec,
     uint32_t* counts, uint32_t* ranges, uint32_t* agg, uint32_t* big_tiles, uint32_t* big_elem,
     uint32_t* big_chunk, ViewScalars* sc, unsigned long long* entries, unsigned long long* tmp,
-    uint32_t* sorted_idx, uint32_t* __restrict__ dbg_key, uint32_t* __restrict__ dbg_tiles) {
+    uint32_t* sorted_idx, uint32_t* __restrict__ dbg_key, uint32_t* __restrict__ dbg_tiles,
+    float* __restrict__ feat_out) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned long long s[kBigChunk];
@@ -574,11 +611,17 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_bilinear(
     if (i >= N) continue;
     Proj p;
     Foot f;
-    const bool vis = project_point(cam, __ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2), p);
+    const float X = __ldg(xyz + 3 * i), Y = __ldg(xyz + 3 * i + 1), Z = __ldg(xyz + 3 * i + 2);
+    const bool vis = project_point(cam, X, Y, Z, p);
     const bool ok = vis && foot_bilinear(g, p.u, p.v, f);
     PointRec pr;
     pr.a = make_float4(p.u, p.v, ok ? p.zc : 0.0f, __ldg(opacity + i));
-    pr.b = pack ? __ldg(reinterpret_cast<const float4*>(feat) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    pr.b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (g.flags & kFlagSH) {
+      if (ok) sh_point_features(cam, g, feat, i, X, Y, Z, pack, pr.b, feat_out);
+    } else if (pack) {
+      pr.b = __ldg(reinterpret_cast<const float4*>(feat) + i);
+    }
     rec[i] = pr;
     if (dbg_key) {
       dbg_key[i] = vis ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
@@ -894,11 +937,22 @@ __device__ __forceinline__ void blend_pixel(const ChunkSmem<CMAX>& cs, const Dev
 }
 
 template <int CMAX>
-__device__ __forceinline__ void write_pixel(const DevCfg& g, const BlendOut& out,
+__device__ __forceinline__ void write_pixel(const DevCam& cam, const DevCfg& g, const BlendOut& out,
                                             const float* __restrict__ bg, int px, int py,
                                             PixFwd<CMAX>& s) {
   const size_t pix = (size_t)py * g.W + px;
-  if (bg) {
+  if (bg && (g.flags & kFlagEnv)) {  // NEXT f2: environment-map background
+    int id[4];
+    float w[4];
+    env_weights(cam, g, px, py, id, w);
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c)
+      if (c < g.C) {
+        const float b = (w[0] * __ldg(bg + (size_t)id[0] * g.C + c) + w[1] * __ldg(bg + (size_t)id[1] * g.C + c)) +
+                        (w[2] * __ldg(bg + (size_t)id[2] * g.C + c) + w[3] * __ldg(bg + (size_t)id[3] * g.C + c));
+        s.F[c] += s.T * b;
+      }
+  } else if (bg) {
 #pragma unroll
     for (int c = 0; c < CMAX; ++c)
       if (c < g.C) s.F[c] += s.T * __ldg(bg + pix * g.C + c);
@@ -970,8 +1024,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_fwd(
     __syncwarp();
     if (!count && __all_sync(0xffffffffu, a.done && b.done)) break;
   }
-  if (inA) write_pixel<CMAX>(g, out, bg, px, pyA, a);
-  if (inB) write_pixel<CMAX>(g, out, bg, px, pyB, b);
+  if (inA) write_pixel<CMAX>(cam, g, out, bg, px, pyA, a);
+  if (inB) write_pixel<CMAX>(cam, g, out, bg, px, pyB, b);
 }
 
 // ---------------------------------------------------------------- H8
@@ -993,7 +1047,7 @@ struct PixBwd {
 };
 
 template <int MODE, int CMAX>
-__device__ __forceinline__ void load_pixel_bwd(const DevCfg& g, const BwdIn& in,
+__device__ __forceinline__ void load_pixel_bwd(const DevCam& cam, const DevCfg& g, const BwdIn& in,
                                                const float* __restrict__ bg, bool inside, int px,
                                                int py, float* Gs, PixBwd<CMAX>& s) {
   s.T = 1.0f;
@@ -1008,10 +1062,11 @@ __device__ __forceinline__ void load_pixel_bwd(const DevCfg& g, const BwdIn& in,
     s.T = in.T_final[pix];
     if (in.gA) s.GA = in.gA[pix];
     if (in.gD) s.GD = in.gD[pix];
+    const bool env = bg && (g.flags & kFlagEnv);
     if (CMAX == 4 && g.C == 4) {
       float4 v = __ldg(reinterpret_cast<const float4*>(in.gF) + pix);
       s.G[0] = v.x; s.G[1] = v.y; s.G[2] = v.z; s.G[3] = v.w;
-      if (bg) {  // S starts as G . bg: the background is behind every fragment
+      if (bg && !env) {  // S starts as G . bg: the background is behind every fragment
         float4 r = __ldg(reinterpret_cast<const float4*>(bg) + pix);
         s.S = (v.x * r.x + v.y * r.y) + (v.z * r.z + v.w * r.w);
       }
@@ -1020,7 +1075,19 @@ __device__ __forceinline__ void load_pixel_bwd(const DevCfg& g, const BwdIn& in,
       for (int c = 0; c < CMAX; ++c)
         if (c < g.C) {
           s.G[c] = in.gF[pix * g.C + c];
-          if (bg) s.S += s.G[c] * bg[pix * g.C + c];
+          if (bg && !env) s.S += s.G[c] * bg[pix * g.C + c];
+        }
+    }
+    if (env) {  // NEXT f2: the environment lookup is the background
+      int id[4];
+      float w[4];
+      env_weights(cam, g, px, py, id, w);
+#pragma unroll
+      for (int c = 0; c < CMAX; ++c)
+        if (c < g.C) {
+          const float b = (w[0] * __ldg(bg + (size_t)id[0] * g.C + c) + w[1] * __ldg(bg + (size_t)id[1] * g.C + c)) +
+                          (w[2] * __ldg(bg + (size_t)id[2] * g.C + c) + w[3] * __ldg(bg + (size_t)id[3] * g.C + c));
+          s.S += s.G[c] * b;
         }
     }
   }
@@ -1110,8 +1177,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_bwd(
   const bool inA = px < g.W && pyA < g.H, inB = px < g.W && pyB < g.H;
   const uint32_t begin = ranges[tile];
   PixBwd<CMAX> a, b;
-  load_pixel_bwd<MODE, CMAX>(g, in, bg, inA, px, pyA, &S.Gs[lane][0], a);
-  load_pixel_bwd<MODE, CMAX>(g, in, bg, inB, px, pyB, &S.Gs[lane + 32][0], b);
+  load_pixel_bwd<MODE, CMAX>(cam, g, in, bg, inA, px, pyA, &S.Gs[lane][0], a);
+  load_pixel_bwd<MODE, CMAX>(cam, g, in, bg, inB, px, pyB, &S.Gs[lane + 32][0], b);
   uint32_t tmax = max(a.last, b.last);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));

@@ -15,6 +15,7 @@ struct DevCam {
   float R[9];
   float t[3];
   float fx, fy, cx, cy, z_near;
+  float cw[3];  // camera centre in world space, -R^T t (SH view directions)
 };
 
 struct DevCfg {
@@ -22,10 +23,13 @@ struct DevCfg {
   float sigma, dil, amax, tmin;
   int tiles_x, tiles_y, ty0, ty1;
   unsigned flags;
+  int env_h, env_w;
 };
 
 constexpr unsigned kFlagSigmaPx = 1u;
 constexpr unsigned kFlagSkipZero = 2u;
+constexpr unsigned kFlagSH = 4u;
+constexpr unsigned kFlagEnv = 8u;
 
 struct Proj {
   float xc, yc, zc, u, v, xz, yz;
@@ -127,6 +131,66 @@ __device__ __forceinline__ float gauss_q(float ca, float cb, float cc, float u, 
   return __fadd_rn(__fadd_rn(__fmul_rn(__fmul_rn(ca, dx), dx),
                              __fmul_rn(__fmul_rn(__fmul_rn(cb, dx), dy), 2.0f)),
                    __fmul_rn(__fmul_rn(cc, dy), dy));
+}
+
+// ---- NEXT f1: degree-2 SH features, values only (no decisions).
+// Real basis, standard constants; d = unit vector camera centre -> point (R26).
+__device__ __forceinline__ void sh_basis(float x, float y, float z, float* Y) {
+  const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+  Y[0] = C0;
+  Y[1] = -C1 * y;
+  Y[2] = C1 * z;
+  Y[3] = -C1 * x;
+  Y[4] = 1.0925484305920792f * x * y;
+  Y[5] = -1.0925484305920792f * y * z;
+  Y[6] = 0.31539156525252005f * (2.0f * z * z - x * x - y * y);
+  Y[7] = -1.0925484305920792f * x * z;
+  Y[8] = 0.5462742152960396f * (x * x - y * y);
+}
+
+__device__ __forceinline__ void sh_dir_basis(const DevCam& c, float X, float Y, float Z, float* B) {
+  const float dx = X - c.cw[0], dy = Y - c.cw[1], dz = Z - c.cw[2];
+  const float n2 = dx * dx + dy * dy + dz * dz;
+  const float inv = n2 > 0.0f ? rsqrtf(n2) : 0.0f;
+  sh_basis(dx * inv, dy * inv, dz * inv, B);
+}
+
+// f_c = sum_k sh[c*9 + k] B_k for the point's coefficient block sh [C, 9]
+__device__ __forceinline__ float sh_feature(const float* __restrict__ sh, int c, const float* B) {
+  float f = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) f += __ldg(sh + c * 9 + k) * B[k];
+  return f;
+}
+
+// ---- NEXT f2: equirectangular environment background (R27).
+// Pixel-centre ray rotated to world space (recomputed: 10 flops instead of
+// the paper's cached direction buffer, 12 B/pixel of HBM on B200);
+// u = (atan2(dx, dz)/2pi + 1/2) We, v = acos(dy)/pi He, texel centres at
+// +1/2, bilinear with azimuthal wrap and polar clamp.
+__device__ __forceinline__ void env_weights(const DevCam& c, const DevCfg& g, int px, int py,
+                                            int* idx4, float* w4) {
+  const float xc = ((float)px + 0.5f - c.cx) / c.fx, yc = ((float)py + 0.5f - c.cy) / c.fy;
+  const float inv = rsqrtf(xc * xc + yc * yc + 1.0f);
+  float d[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) d[k] = (c.R[k] * xc + c.R[3 + k] * yc + c.R[6 + k]) * inv;
+  const float PI = 3.14159265358979323846f;
+  const float u = (atan2f(d[0], d[2]) * (0.5f / PI) + 0.5f) * g.env_w;
+  const float v = acosf(fminf(fmaxf(d[1], -1.0f), 1.0f)) * (1.0f / PI) * g.env_h;
+  const float x = u - 0.5f, y = v - 0.5f;
+  const float fx0 = floorf(x), fy0 = floorf(y);
+  const float a = x - fx0, b = y - fy0;
+  int i0 = (int)fx0, j0 = (int)fy0;
+  int i1 = i0 + 1, j1 = j0 + 1;
+  i0 = ((i0 % g.env_w) + g.env_w) % g.env_w;
+  i1 = ((i1 % g.env_w) + g.env_w) % g.env_w;
+  j0 = min(max(j0, 0), g.env_h - 1);
+  j1 = min(max(j1, 0), g.env_h - 1);
+  idx4[0] = j0 * g.env_w + i0; w4[0] = (1.0f - a) * (1.0f - b);
+  idx4[1] = j0 * g.env_w + i1; w4[1] = a * (1.0f - b);
+  idx4[2] = j1 * g.env_w + i0; w4[2] = (1.0f - a) * b;
+  idx4[3] = j1 * g.env_w + i1; w4[3] = a * b;
 }
 
 }  // namespace inpc

@@ -58,9 +58,9 @@ def test_status_strings_and_null_ctx(m):
 
 
 def test_struct_layouts_match_header(m):
-    # inpc_camera: 9+3+5 floats; inpc_raster_cfg: 4 ints, 4 floats, 2 ints, 1 uint
+    # inpc_camera: 9+3+5 floats; inpc_raster_cfg: 4 ints, 4 floats, 2 ints, 1 uint, 2 ints
     assert ct.sizeof(m.Camera) == 17 * 4
-    assert ct.sizeof(m.RasterCfg) == 11 * 4
+    assert ct.sizeof(m.RasterCfg) == 13 * 4
 
 
 def test_no_oracle_in_product_path():

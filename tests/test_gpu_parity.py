@@ -288,3 +288,66 @@ def test_unfused_binning_cfg2(inpc, ctx_unfused):
 
 def test_unfused_big_tile(inpc, ctx_unfused):
     test_one_hot_tile_over_smem_cap(inpc, ctx_unfused, 5000)
+
+
+# ------------------------------------------------------------------ NEXT f1 / f2
+def _sh_case(seed, C=4, N=1000, mode="bilinear"):
+    c = synthgen.config1(seed=seed, N=N, C=C)
+    cam = synthgen.camera(np.eye(3), [0.1, -0.05, 0.2], 64, 64, 32, 32, 0.1)   # centre off origin
+    c["cams"] = [cam]
+    sh = np.random.default_rng(seed + 7).normal(0, 0.5, (N, C, 9)).astype(np.float32)
+    return c, sh
+
+
+@pytest.mark.parametrize("C,mode,kw", [(4, "bilinear", {}), (3, "bilinear", {}),
+                                       (4, "gaussian", dict(sigma=0.6, flags=1))])
+def test_sh_features_fwd_bwd(inpc, ctx, C, mode, kw):
+    """f1: SH degree-2 features evaluated in the projection kernel:
+    image against the oracle fed with oracle-evaluated features; dL/dcoeff
+    against the oracle's dL/df times the oracle's basis."""
+    c, sh = _sh_case(40 + C, C)
+    cam, H, W = c["cams"][0], c["H"], c["W"]
+    f_or, Y = oracle.sh_features(cam, c["xyz"], sh)
+    kw2 = dict(kw)
+    flags = inpc.FLAG_SH_FEATURES | kw2.pop("flags", 0)
+    cfg = inpc.make_cfg(H, W, C, mode, flags=flags | inpc.FLAG_DEBUG, **kw2)
+    xyz, op, sht = dev(c["xyz"]), dev(c["opacity"]), dev(sh)
+    out = ctx.forward(cfg, c["cams"], xyz, sht, op, debug_counts=True)
+    okw = dict(kw2, flags=kw.get("flags", 0))
+    r = oracle.render(cam, c["xyz"], f_or, c["opacity"], H, W, mode=mode, **okw)
+    ok = out["ncontrib"][0].cpu().numpy() == r["n_contrib"]
+    assert (~ok).sum() <= 2
+    np.testing.assert_allclose(out["F"][0].cpu().numpy()[ok], r["F"][ok], atol=IMG_TOL)
+    gF, gA, gD = (x[0] for x in synthgen.upstream_grads(3, 1, H, W, C))
+    gsh, go = ctx.backward(cfg, c["cams"], xyz, sht, op, dev(gF), dev(gA), dev(gD))
+    torch.cuda.synchronize()
+    o = oracle.backward(cam, c["xyz"], f_or, c["opacity"], H, W, gF, gA, gD, mode=mode, **okw)
+    g_sh_or = o["g_feat"][:, :, None] * Y[:, None, :]
+    check_grads(gsh.cpu().numpy(), g_sh_or)
+    check_grads(go.cpu().numpy(), o["g_opacity"])
+
+
+def test_env_background_fwd_bwd(inpc, ctx):
+    """f2: equirectangular environment background composited in the blend
+    epilogue against the oracle fed with the oracle's
+    per-pixel lookup."""
+    c = synthgen.config1(seed=55)
+    R = synthgen.random_rotation(np.random.default_rng(5))
+    c["cams"] = [synthgen.camera(R, [0, 0, 0], 64, 64, 32, 32, 0.1)]
+    xyz_cam = c["xyz"].astype(np.float64)
+    c["xyz"] = (xyz_cam @ R).astype(np.float32)   # same camera-space cloud, rotated world
+    cam, H, W, C = c["cams"][0], c["H"], c["W"], c["C"]
+    env = np.random.default_rng(6).uniform(-1, 1, (32, 64, C)).astype(np.float32)
+    bg = oracle.env_background(cam, env, H, W)
+    cfg = inpc.make_cfg(H, W, C, env_hw=env.shape[:2], flags=inpc.FLAG_DEBUG)
+    xyz, feat, op, envt = dev(c["xyz"]), dev(c["feat"]), dev(c["opacity"]), dev(env)
+    out = ctx.forward(cfg, c["cams"], xyz, feat, op, bg=envt, debug_counts=True)
+    r = oracle.render(cam, c["xyz"], c["feat"], c["opacity"], H, W, bg=bg)
+    np.testing.assert_array_equal(out["ncontrib"][0].cpu().numpy(), r["n_contrib"])
+    np.testing.assert_allclose(out["F"][0].cpu().numpy(), r["F"], atol=IMG_TOL)
+    gF, gA, gD = (x[0] for x in synthgen.upstream_grads(4, 1, H, W, C))
+    gf, go = ctx.backward(cfg, c["cams"], xyz, feat, op, dev(gF), dev(gA), dev(gD), bg=envt)
+    torch.cuda.synchronize()
+    o = oracle.backward(cam, c["xyz"], c["feat"], c["opacity"], H, W, gF, gA, gD, bg=bg)
+    check_grads(gf.cpu().numpy(), o["g_feat"])
+    check_grads(go.cpu().numpy(), o["g_opacity"])
