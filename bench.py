@@ -33,6 +33,7 @@ import synthgen  # noqa: E402
 
 METRIC = "frames/s and Mpoints/s at 1080p fwd+bwd, % of B200 HBM roofline, 1/2/4/8 GPUs"
 WORKLOAD = "cfg2: 2^20-point view-specific cloud, 1920x1080, C=4, bilinear 2x2 splats, fwd+bwd"
+WORKLOAD5 = "cfg5: 64 orbit views of a 2^23-point cloud, 1920x1080, C=4, bilinear, fwd+bwd, shared features"
 NOMINAL_HBM_GBS = 8000.0
 
 
@@ -45,19 +46,30 @@ def peaks():
 
 
 # ------------------------------------------------------------------ byte model
-def algorithmic_bytes(N, Nv, Ft, P, C):
+def algorithmic_bytes(N, Nv, Ft, P, C, sh=False, env=False):
     """Compulsory bytes per stage: each datum the method must
-    move, counted once, whatever the implementation re-reads."""
-    return {
-        "project_count": 12 * N,                       # positions
+    move, counted once, whatever the implementation re-reads.  (Sums over
+    views: N, Nv, Ft, P are totals.)  sh: features come as 9 SH coefficients
+    per channel (read 36 C B per visible point, gradient written 36 C B);
+    env: a C-channel background value per pixel, read in fwd and bwd."""
+    fbytes = (36 if sh else 4) * C
+    m = {
+        "project_count": 12 * N + (fbytes * Nv if sh else 0),   # positions (+ SH coefficients)
         "scan_tiles": 0,
         "scatter": 8 * Ft,                             # one write of the (key, idx) record
         "sort_big": 0,
-        "blend_fwd": 8 * Ft + (4 + 4 * C) * Nv + 4 * P * (C + 2) + 8 * P,
+        "blend_fwd": 8 * Ft + (4 + (0 if sh else 4 * C)) * Nv + 4 * P * (C + 2) + 8 * P,
         #            record read, opacity+features, F/A/D write, T_final+last write
         "blend_bwd": 4 * P * (C + 2) + 8 * P + 4 * Ft + (16 + 4 * C) * Nv + 4 * (C + 1) * Nv,
         #            upstream grads, saved state, sorted idx, xyz/o/f, gradient write
     }
+    if sh:
+        m["sh_grad"] = 12 * Nv + fbytes * Nv           # positions (directions) + coefficient gradients
+    if env:
+        m["blend_fwd"] += 4 * C * P
+        m["blend_bwd"] += 4 * C * P
+    m["bin_fused"] = m["project_count"] + m["scatter"]
+    return m
 
 
 # ------------------------------------------------------------------ clocks
@@ -175,39 +187,73 @@ def run_ours(args, rank, world, local_rank):
 
     import paper_2508_19140_b200 as inpc
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    c = synthgen.config2(seed=2 + rank)
+    dev_index = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    if args.config == 5:
+        # training-style view batch (configs[4]): 64 orbit views of a 2^23
+        # cloud, shared features, views split over ranks, gradients all-reduced
+        c = synthgen.config5()
+        views = [v for v in range(64) if v * world // 64 == rank]   # contiguous blocks
+        cams = [c["cams"][v] for v in views]
+        seed_g = 5 + rank
+    else:
+        c = synthgen.config2(seed=2 + rank)
+        cams = c["cams"]
+        seed_g = 2 + rank
+    V = len(cams)
     H, W, C = c["H"], c["W"], c["C"]
     N = c["xyz"].shape[0]
     P = H * W
+    flags = 0
+    feat_np = c["feat"]
+    if args.variant in ("sh", "sh+env"):
+        flags |= inpc.FLAG_SH_FEATURES
+        feat_np = np.random.default_rng(seed_g + 11).normal(0, 0.5, (N, C, 9)).astype(np.float32)
+    env_hw = None
+    env_t = None
+    if args.variant in ("env", "sh+env"):
+        env_hw = (1024, 2048)   # the paper's distilled map size
+        env_t = torch.from_numpy(np.random.default_rng(seed_g + 12).uniform(
+            -1, 1, (1024, 2048, C)).astype(np.float32)).to(dev)
     xyz_h = torch.from_numpy(c["xyz"]).pin_memory()
-    feat_h = torch.from_numpy(c["feat"]).pin_memory()
+    feat_h = torch.from_numpy(feat_np).pin_memory()
     op_h = torch.from_numpy(c["opacity"]).pin_memory()
-    gF_h, gA_h, gD_h = (torch.from_numpy(x).pin_memory() for x in synthgen.upstream_grads(2 + rank, 1, H, W, C))
     xyz, feat, op = xyz_h.to(dev), feat_h.to(dev), op_h.to(dev)
+    if args.config == 5:
+        # one (V, H, W) block of upstream gradients shared by the rank's views
+        g1 = [torch.from_numpy(x) for x in synthgen.upstream_grads(seed_g, 1, H, W, C)]
+        gF_h, gA_h, gD_h = (x.expand((V,) + tuple(x.shape[1:])).contiguous().pin_memory() for x in g1)
+    else:
+        gF_h, gA_h, gD_h = (torch.from_numpy(x).pin_memory() for x in synthgen.upstream_grads(seed_g, 1, H, W, C))
     gF, gA, gD = gF_h.to(dev), gA_h.to(dev), gD_h.to(dev)
-    ctx = inpc.Context(local_rank)
-    cfg = inpc.make_cfg(H, W, C, "bilinear")
-    cams = c["cams"]
-    out = dict(F=torch.empty((1, H, W, C), device=dev), A=torch.empty((1, H, W), device=dev),
-               D=torch.empty((1, H, W), device=dev))
+    ctx = inpc.Context(dev_index)
+    cfg = inpc.make_cfg(H, W, C, "bilinear", flags=flags, env_hw=env_hw)
+    out = dict(F=torch.empty((V, H, W, C), device=dev), A=torch.empty((V, H, W), device=dev),
+               D=torch.empty((V, H, W), device=dev))
     g_feat = torch.zeros_like(feat)
     g_op = torch.zeros_like(op)
+    reduce_grads = args.config == 5 and world > 1
 
     def step():
         g_feat.zero_()
         g_op.zero_()
-        ctx.forward(cfg, cams, xyz, feat, op, out=out)
-        ctx.backward(cfg, cams, xyz, feat, op, gF, gA, gD, g_feat=g_feat, g_opacity=g_op)
+        ctx.forward(cfg, cams, xyz, feat, op, bg=env_t, out=out)
+        ctx.backward(cfg, cams, xyz, feat, op, gF, gA, gD, bg=env_t, g_feat=g_feat, g_opacity=g_op)
+        if reduce_grads:   # the view batch's one exchange step (shared features, R20)
+            dist.all_reduce(g_feat)
+            dist.all_reduce(g_op)
 
-    # workload statistics (untimed): visible points, tile entries
-    dbg = inpc.make_cfg(H, W, C, "bilinear", flags=inpc.FLAG_DEBUG)
-    ctx.forward(dbg, cams, xyz, feat, op)
-    ex = ctx.debug_export(0, N=N, H=H, W=W)
-    Nv = int((ex["tiles_touched"] > 0).sum().item())
-    Ft = int(ex["F_t"])
-    model = algorithmic_bytes(N, Nv, Ft, P, C)
+    # workload statistics (untimed): visible points, tile entries, per view
+    dbg = inpc.make_cfg(H, W, C, "bilinear", flags=flags | inpc.FLAG_DEBUG, env_hw=env_hw)
+    ctx.forward(dbg, cams, xyz, feat, op, bg=env_t)
+    Nv = Ft = 0
+    for v in range(V):
+        ex = ctx.debug_export(v, N=N, H=H, W=W)
+        Nv += int((ex["tiles_touched"] > 0).sum().item())
+        Ft += int(ex["F_t"])
+    model = algorithmic_bytes(N * V, Nv, Ft, P * V, C, sh="sh" in args.variant,
+                              env="env" in args.variant)
     step_bytes = sum(model.values())
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -279,8 +325,8 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     ms_per_step = tot_ms / args.steps
-    frames = world * args.steps
-    fps = frames / (tot_ms / 1e3)
+    frames_per_step = 64 if args.config == 5 else world
+    fps = frames_per_step * args.steps / (tot_ms / 1e3)
     # our kernels launched inside the timed region: the profiled eager steps
     # (counted by the library) plus, with a graph, the kernels of each replay
     launches = int(sum(v[1] for v in stages.values())) + (graph_launches * args.steps if graph_used else 0)
@@ -290,7 +336,7 @@ def run_ours(args, rank, world, local_rank):
     kern = {k: v for k, v in stages.items() if v[1] > 0}
     dom = max(kern, key=lambda k: kern[k][0])
     dom_ms = kern[dom][0] / kern[dom][1]
-    dom_bytes = model.get(dom, 0)
+    dom_bytes = model.get(dom, 0) / max(1, round(kern[dom][1] / args.steps))   # per launch (per view)
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
@@ -303,9 +349,9 @@ def run_ours(args, rank, world, local_rank):
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
 
     # end to end through the public API with host (pinned) buffers
-    F_h = torch.empty((1, H, W, C), pin_memory=True)
-    A_h = torch.empty((1, H, W), pin_memory=True)
-    D_h = torch.empty((1, H, W), pin_memory=True)
+    F_h = torch.empty((V, H, W, C), pin_memory=True)
+    A_h = torch.empty((V, H, W), pin_memory=True)
+    D_h = torch.empty((V, H, W), pin_memory=True)
     gf_h = torch.empty_like(feat_h).pin_memory()
     go_h = torch.empty_like(op_h).pin_memory()
     h2d = sum(t.numel() * 4 for t in (xyz_h, feat_h, op_h, gF_h, gA_h, gD_h))
@@ -340,11 +386,12 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_fps = world / (e2e_ms / 1e3)
+    e2e_fps = frames_per_step / (e2e_ms / 1e3)
 
     # CPU oracle baseline (rank 0, N = 1 only): bounded sample of the same workload
     cpu = None
-    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.profile_run):
+    if (rank == 0 and world == 1 and args.config == 2 and args.variant == "base"
+            and not (args.no_cpu_baseline or args.profile_run)):
         th = cpu_threads()
         gFn, gAn, gDn = (x[0] for x in synthgen.upstream_grads(2, 1, H, W, C))
         tt, ff = 0.0, 0.0
@@ -359,11 +406,14 @@ def run_ours(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": WORKLOAD, "N": N, "N_visible": Nv, "F_t": Ft, "H": H, "W": W,
+            "higher_is_better": True, "scaling": "strong" if args.config == 5 else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD5 if args.config == 5 else WORKLOAD,
+                       "variant": args.variant, "N": N, "views_per_rank": V,
+                       "N_visible": Nv, "F_t": Ft, "H": H, "W": W,
                        "C": C, "mode": "bilinear", "alpha_max": 0.99, "t_min": 1e-4,
-                       "parallelism": f"independent frames x{world} (weak)",
+                       "parallelism": (f"64 views split over {world} ranks + gradient all-reduce"
+                                       if args.config == 5 else f"independent frames x{world} (weak)"),
                        "l2": "flushed: 256 MiB write between steps, outside the per-step events"},
             "mpoints_per_s": fps * N / 1e6,
             "step_algorithmic_bytes": step_bytes,
@@ -394,6 +444,12 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
+    ap.add_argument("--config", type=int, choices=[2, 5], default=2,
+                    help="2: cfg2 frame per rank (default, weak scaling); 5: 64-view batch split "
+                         "over ranks with a gradient all-reduce (strong scaling)")
+    ap.add_argument("--variant", choices=["base", "sh", "env", "sh+env"], default="base",
+                    help="NEXT rows: SH-coefficient features (f1) / env-map background (f2)")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (GPUs) or gloo (1-GPU tests)")
     ap.add_argument("--profile-run", action="store_true",
                     help="for ncu: no clock ramp, no e2e leg, no CPU baseline")
     args = ap.parse_args()
@@ -407,8 +463,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev_index = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(dev_index)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(args.dist_backend)
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
