@@ -351,9 +351,9 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
   c->big_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
   {
     int o2 = 0, o4 = 0, o8 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_bin_bilinear<2>, kBinThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k_bin_bilinear<4>, kBinThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o8, k_bin_bilinear<8>, kBinThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_bin_bilinear<2, false>, kBinThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k_bin_bilinear<4, false>, kBinThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o8, k_bin_bilinear<8, false>, kBinThreads, 0);
     c->bin_grid[0] = c->num_sms * o2;
     c->bin_grid[1] = c->num_sms * o4;
     c->bin_grid[2] = c->num_sms * o8;
@@ -537,7 +537,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     int fused_kp = 0, fused_grid = 0;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cap);
-    if (!gauss && N > 0 && !c->no_fused_bin && cap == cudaStreamCaptureStatusNone) {
+    if (!gauss && !sh && N > 0 && !c->no_fused_bin && cap == cudaStreamCaptureStatusNone) {
       const int kps[3] = {2, 4, 8};
       for (int q = 0; q < 3; ++q)
         if (c->bin_grid[q] > 0 && N <= (int64_t)kps[q] * c->bin_grid[q] * kBinThreads) {
@@ -572,20 +572,27 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
                       (void*)&Nn, (void*)&Ti, (void*)&recp, (void*)&tc, (void*)&rg, (void*)&ag,
                       (void*)&bt, (void*)&be, (void*)&bc, (void*)&sc, (void*)&en, (void*)&tp,
                       (void*)&si, (void*)&dk, (void*)&dt, (void*)&feat_out};
-      void* fn = fused_kp == 2 ? (void*)k_bin_bilinear<2> : fused_kp == 4 ? (void*)k_bin_bilinear<4>
-                                                                          : (void*)k_bin_bilinear<8>;
+      void* fn = fused_kp == 2 ? (void*)k_bin_bilinear<2, false>
+                 : fused_kp == 4 ? (void*)k_bin_bilinear<4, false>
+                                 : (void*)k_bin_bilinear<8, false>;
       CK(cudaLaunchCooperativeKernel(fn, fused_grid, kBinThreads, args, 0, s));
     }
     if (N > 0 && !fused_kp) {
       StageTimer tm(c, s, kStProject, 1);
-      if (gauss)
-        k_project_count<1><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N,
-                                                           (PointRec*)vs.rec.p, tc, nullptr, dk, dt,
-                                                           feat_out);
+      PointRec* recp = (PointRec*)vs.rec.p;
+      uint4* slp = (uint4*)c->slots.p;
+      if (gauss && sh)
+        k_project_count<1, true><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N, recp,
+                                                                 tc, nullptr, dk, dt, feat_out);
+      else if (gauss)
+        k_project_count<1, false><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N, recp,
+                                                                  tc, nullptr, dk, dt, feat_out);
+      else if (sh)
+        k_project_count<0, true><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N, recp,
+                                                                 tc, slp, dk, dt, feat_out);
       else
-        k_project_count<0><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N,
-                                                           (PointRec*)vs.rec.p, tc, (uint4*)c->slots.p,
-                                                           dk, dt, feat_out);
+        k_project_count<0, false><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N, recp,
+                                                                  tc, slp, dk, dt, feat_out);
       CK(cudaGetLastError());
     }
     if (!fused_kp) {
@@ -748,7 +755,7 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     }
     if (sh) {
       StageTimer tm(c, s, kStShGrad, 1);
-      k_sh_grad<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(dc, g, xyz, N, (const float*)c->g_eval.p,
+      k_sh_grad<<<(unsigned)((N + kShPts - 1) / kShPts), 256, 0, s>>>(dc, g, xyz, N, (const float*)c->g_eval.p,
                                                             g_point_feat + (size_t)v * feat_view_stride);
       CK(cudaGetLastError());
     }

@@ -27,7 +27,7 @@ namespace inpc {
 
 constexpr int kWarpsPerBlock = 4;    // blend kernels: one warp per tile
 constexpr int kWarpSortCap = 256;    // tiles above this go through k_sort_big
-constexpr int kBigChunk = 2048;      // chunk of k_sort_big's SMEM sort
+constexpr int kBigChunk = 2048;      // chunk of k_sort_big's SMEM sort (16 KB of keys)
 constexpr int kBigThreads = 512;
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;        // tiles per scan thread
@@ -57,34 +57,58 @@ __device__ __forceinline__ void sh_point_features(const DevCam& cam, const DevCf
   sh_dir_basis(cam, X, Y, Z, B);
   const float* shi = sh + (size_t)i * g.C * 9;
   if (packed) {
-    F = make_float4(sh_feature(shi, 0, B), sh_feature(shi, 1, B), sh_feature(shi, 2, B),
-                    sh_feature(shi, 3, B));
+    // 36 coefficients = 9 aligned float4 (144 B per point)
+    float q[36];
+    const float4* s4 = reinterpret_cast<const float4*>(shi);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const float4 v = __ldg(s4 + k);
+      q[4 * k] = v.x; q[4 * k + 1] = v.y; q[4 * k + 2] = v.z; q[4 * k + 3] = v.w;
+    }
+    float f[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      f[c] = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) f[c] += q[c * 9 + k] * B[k];
+    }
+    F = make_float4(f[0], f[1], f[2], f[3]);
   } else {
     for (int c = 0; c < g.C; ++c) feat_out[(size_t)i * g.C + c] = sh_feature(shi, c, B);
   }
 }
 
 // NEXT f1 backward: dL/dcoeff[c][k] += dL/df_c Y_k(d)  (g_sh [N, C, 9]).
+// A block handles 32 points: their basis values and dL/df are staged in SMEM
+// and the 32*C*9 contiguous coefficient gradients are read-modify-written
+// with consecutive threads on consecutive floats (coalesced).
+constexpr int kShPts = 32;
 __global__ void __launch_bounds__(256) k_sh_grad(DevCam cam, DevCfg g, const float* __restrict__ xyz,
                                                  int64_t N, const float* __restrict__ g_f,
                                                  float* __restrict__ g_sh) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  float B[9];
-  sh_dir_basis(cam, __ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2), B);
-  for (int c = 0; c < g.C; ++c) {
-    const float gf = __ldg(g_f + (size_t)i * g.C + c);
-    if (gf == 0.0f) continue;
-    float* o = g_sh + ((size_t)i * g.C + c) * 9;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) o[k] += gf * B[k];
+  __shared__ float sB[kShPts][9];
+  __shared__ float sG[kShPts * 64];
+  const int64_t p0 = (int64_t)blockIdx.x * kShPts;
+  const int np = (int)min((int64_t)kShPts, N - p0);
+  if (threadIdx.x < np) {
+    const int64_t i = p0 + threadIdx.x;
+    sh_dir_basis(cam, __ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2), sB[threadIdx.x]);
+  }
+  for (int j = threadIdx.x; j < np * g.C; j += blockDim.x) sG[j] = __ldg(g_f + p0 * g.C + j);
+  __syncthreads();
+  const int per_pt = g.C * 9;
+  float* out = g_sh + p0 * per_pt;
+  for (int j = threadIdx.x; j < np * per_pt; j += blockDim.x) {
+    const int p = j / per_pt, r = j - p * per_pt, c = r / 9, k = r - c * 9;
+    const float gf = sG[p * g.C + c];
+    if (gf != 0.0f) out[j] += gf * sB[p][k];
   }
 }
 
 // kPPT points per thread, loads of all of them issued before any compute so
 // enough bytes are in flight to cover HBM latency.
-template <int MODE>
-__global__ void __launch_bounds__(kPointThreads) k_project_count(
+template <int MODE, bool SH>
+__global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
     DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ opacity,
     const float* __restrict__ feat, bool pack, int64_t N, PointRec* __restrict__ rec,
     uint32_t* __restrict__ tile_count, uint4* __restrict__ slots, uint32_t* __restrict__ dbg_key,
@@ -101,7 +125,7 @@ __global__ void __launch_bounds__(kPointThreads) k_project_count(
       Y[k] = __ldg(xyz + 3 * i + 1);
       Z[k] = __ldg(xyz + 3 * i + 2);
       O[k] = __ldg(opacity + i);
-      if (MODE == 0 && pack && !(g.flags & kFlagSH)) Fv[k] = __ldg(reinterpret_cast<const float4*>(feat) + i);
+      if (MODE == 0 && pack && !SH) Fv[k] = __ldg(reinterpret_cast<const float4*>(feat) + i);
     }
   }
 #pragma unroll
@@ -117,8 +141,7 @@ __global__ void __launch_bounds__(kPointThreads) k_project_count(
       if (MODE == 0) ok = foot_bilinear(g, p.u, p.v, f);
       else ok = gauss_conic(cam, g, p, ca, cb, cc, r) && gauss_rect(g, p.u, p.v, r, f);
     }
-    if ((g.flags & kFlagSH) && ok) sh_point_features(cam, g, feat, i, X[k], Y[k], Z[k], MODE == 0 && pack,
-                                                     Fv[k], feat_out);
+    if (SH && ok) sh_point_features(cam, g, feat, i, X[k], Y[k], Z[k], MODE == 0 && pack, Fv[k], feat_out);
     PointRec pr;
     pr.a = make_float4(p.u, p.v, ok ? p.zc : 0.0f, O[k]);
     if (MODE == 0) pr.b = pack ? Fv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -520,9 +543,11 @@ __device__ __forceinline__ void big_sort_body(
     uint32_t c = gch - big_chunk[j];
     uint32_t begin = ranges[t] + c * kBigChunk;
     uint32_t n = min((uint32_t)kBigChunk, ranges[t + 1] - begin);
-    for (int k = threadIdx.x; k < kBigChunk; k += blockDim.x) s[k] = k < (int)n ? entries[begin + k] : ~0ull;
+    int np = 64;  // sort network of the next power of two, not the full chunk
+    while (np < (int)n) np <<= 1;
+    for (int k = threadIdx.x; k < np; k += blockDim.x) s[k] = k < (int)n ? entries[begin + k] : ~0ull;
     __syncthreads();
-    block_bitonic(s, kBigChunk);
+    block_bitonic(s, np);
     for (int k = threadIdx.x; k < (int)n; k += blockDim.x) entries[begin + k] = s[k];
     __syncthreads();
   }
@@ -586,8 +611,8 @@ __global__ void __launch_bounds__(kBigThreads) k_sort_big(
 //   phase 4  H4/H6: tiles over the warp-sort cap (big_sort_body)
 constexpr int kBinThreads = 512;
 
-template <int KP>
-__global__ void __launch_bounds__(kBinThreads) k_bin_bilinear(
+template <int KP, bool SH>
+__global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
     DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ opacity,
     const float* __restrict__ feat, bool pack, int64_t N, int T, PointRec* __restrict__ rec,
     uint32_t* counts, uint32_t* ranges, uint32_t* agg, uint32_t* big_tiles, uint32_t* big_elem,
@@ -617,7 +642,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_bilinear(
     PointRec pr;
     pr.a = make_float4(p.u, p.v, ok ? p.zc : 0.0f, __ldg(opacity + i));
     pr.b = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (g.flags & kFlagSH) {
+    if (SH) {
       if (ok) sh_point_features(cam, g, feat, i, X, Y, Z, pack, pr.b, feat_out);
     } else if (pack) {
       pr.b = __ldg(reinterpret_cast<const float4*>(feat) + i);
@@ -876,6 +901,30 @@ __device__ __forceinline__ bool entry_alpha(const ChunkSmem<CMAX>& cs, const Dev
   }
 }
 
+// Background of pixel (px, py) from the environment map env [He, We, C].
+template <int CMAX>
+__device__ __forceinline__ void env_lookup(const DevCam& cam, const DevCfg& g,
+                                           const float* __restrict__ env, int px, int py, float* b) {
+  int id[4];
+  float w[4];
+  env_weights(cam, g, px, py, id, w);
+  if (CMAX == 4 && g.C == 4) {
+    float4 t[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] = __ldg(reinterpret_cast<const float4*>(env) + id[q]);
+    b[0] = (w[0] * t[0].x + w[1] * t[1].x) + (w[2] * t[2].x + w[3] * t[3].x);
+    b[1] = (w[0] * t[0].y + w[1] * t[1].y) + (w[2] * t[2].y + w[3] * t[3].y);
+    b[2] = (w[0] * t[0].z + w[1] * t[1].z) + (w[2] * t[2].z + w[3] * t[3].z);
+    b[3] = (w[0] * t[0].w + w[1] * t[1].w) + (w[2] * t[2].w + w[3] * t[3].w);
+  } else {
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c)
+      b[c] = c < g.C ? (w[0] * __ldg(env + (size_t)id[0] * g.C + c) + w[1] * __ldg(env + (size_t)id[1] * g.C + c)) +
+                           (w[2] * __ldg(env + (size_t)id[2] * g.C + c) + w[3] * __ldg(env + (size_t)id[3] * g.C + c))
+                     : 0.0f;
+  }
+}
+
 struct BlendOut {
   float* F;           // [H,W,C]
   float* A;           // [H,W] or null
@@ -942,16 +991,11 @@ __device__ __forceinline__ void write_pixel(const DevCam& cam, const DevCfg& g, 
                                             PixFwd<CMAX>& s) {
   const size_t pix = (size_t)py * g.W + px;
   if (bg && (g.flags & kFlagEnv)) {  // NEXT f2: environment-map background
-    int id[4];
-    float w[4];
-    env_weights(cam, g, px, py, id, w);
+    float b[CMAX];
+    env_lookup<CMAX>(cam, g, bg, px, py, b);
 #pragma unroll
     for (int c = 0; c < CMAX; ++c)
-      if (c < g.C) {
-        const float b = (w[0] * __ldg(bg + (size_t)id[0] * g.C + c) + w[1] * __ldg(bg + (size_t)id[1] * g.C + c)) +
-                        (w[2] * __ldg(bg + (size_t)id[2] * g.C + c) + w[3] * __ldg(bg + (size_t)id[3] * g.C + c));
-        s.F[c] += s.T * b;
-      }
+      if (c < g.C) s.F[c] += s.T * b[c];
   } else if (bg) {
 #pragma unroll
     for (int c = 0; c < CMAX; ++c)
@@ -1079,16 +1123,11 @@ __device__ __forceinline__ void load_pixel_bwd(const DevCam& cam, const DevCfg& 
         }
     }
     if (env) {  // NEXT f2: the environment lookup is the background
-      int id[4];
-      float w[4];
-      env_weights(cam, g, px, py, id, w);
+      float b[CMAX];
+      env_lookup<CMAX>(cam, g, bg, px, py, b);
 #pragma unroll
       for (int c = 0; c < CMAX; ++c)
-        if (c < g.C) {
-          const float b = (w[0] * __ldg(bg + (size_t)id[0] * g.C + c) + w[1] * __ldg(bg + (size_t)id[1] * g.C + c)) +
-                          (w[2] * __ldg(bg + (size_t)id[2] * g.C + c) + w[3] * __ldg(bg + (size_t)id[3] * g.C + c));
-          s.S += s.G[c] * b;
-        }
+        if (c < g.C) s.S += s.G[c] * b[c];
     }
   }
 #pragma unroll
@@ -1160,8 +1199,9 @@ __device__ __forceinline__ uint32_t below_mask(uint32_t last, uint32_t base) {
   return k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
 }
 
+// 7 CTAs of 4 warps per SM (<= 73 registers): measured 82 vs 93 us at 6 CTAs on cfg 2
 template <int MODE, int CMAX>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_bwd(
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, CMAX <= 4 ? 7 : 1) k_blend_bwd(
     DevCam cam, DevCfg g, int band_tiles, const PointRec* __restrict__ rec,
     const float* __restrict__ feat, bool packed, const float* __restrict__ bg,
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ sorted_idx, BwdIn in) {

@@ -181,10 +181,10 @@ __device__ __forceinline__ void env_weights(const DevCam& c, const DevCfg& g, in
   const float x = u - 0.5f, y = v - 0.5f;
   const float fx0 = floorf(x), fy0 = floorf(y);
   const float a = x - fx0, b = y - fy0;
-  int i0 = (int)fx0, j0 = (int)fy0;
+  int i0 = (int)fx0, j0 = (int)fy0;  // u in [0, We]: x in [-1/2, We - 1/2]
   int i1 = i0 + 1, j1 = j0 + 1;
-  i0 = ((i0 % g.env_w) + g.env_w) % g.env_w;
-  i1 = ((i1 % g.env_w) + g.env_w) % g.env_w;
+  i0 = i0 < 0 ? i0 + g.env_w : (i0 >= g.env_w ? i0 - g.env_w : i0);  // azimuthal wrap
+  i1 = i1 < 0 ? i1 + g.env_w : (i1 >= g.env_w ? i1 - g.env_w : i1);
   j0 = min(max(j0, 0), g.env_h - 1);
   j1 = min(max(j1, 0), g.env_h - 1);
   idx4[0] = j0 * g.env_w + i0; w4[0] = (1.0f - a) * (1.0f - b);
