@@ -402,6 +402,68 @@ __device__ __forceinline__ void block_bitonic(unsigned long long* s, int np) {
     }
 }
 
+// Compare-exchange steps j = jmax .. 1 (j < 64) of bitonic level k on the
+// 64-element segment held by a warp in registers: element i = seg + 32 r +
+// lane in v[r]; the direction uses the global index i.
+__device__ __forceinline__ void seg_bitonic_low(unsigned long long (&v)[2], int seg, int k, int jmax,
+                                                int lane) {
+  for (int j = jmax; j > 0; j >>= 1) {
+    if (j == 32) {
+      const bool up = ((seg + lane) & k) == 0;  // bit 5 clear for r = 0
+      const unsigned long long a = v[0], b = v[1];
+      const bool sw = (a > b) == up;
+      v[0] = sw ? b : a;
+      v[1] = sw ? a : b;
+    } else {
+      const bool lower = (lane & j) == 0;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], j);
+        const bool up = ((seg + r * 32 + lane) & k) == 0;
+        v[r] = (lower == up) ? (o < v[r] ? o : v[r]) : (o > v[r] ? o : v[r]);
+      }
+    }
+  }
+}
+
+// Block-wide ascending bitonic sort of np (power of two, >= 64) keys in
+// SMEM with most steps in registers: every step with partner distance < 64
+// runs on 64-key warp segments with shuffles, only the steps with distance
+// >= 64 go through SMEM with block barriers (10 of 55 barriers at np = 1024).
+__device__ __forceinline__ void block_bitonic_fast(unsigned long long* s, int np) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // levels k <= 64 entirely in registers
+  for (int seg = wid * 64; seg < np; seg += nw * 64) {
+    unsigned long long v[2] = {s[seg + lane], s[seg + 32 + lane]};
+    for (int k = 2; k <= 64; k <<= 1) seg_bitonic_low(v, seg, k, k >> 1, lane);
+    s[seg + lane] = v[0];
+    s[seg + 32 + lane] = v[1];
+  }
+  __syncthreads();
+  for (int k = 128; k <= np; k <<= 1) {
+    for (int j = k >> 1; j >= 64; j >>= 1) {
+      for (int t = threadIdx.x; t < (np >> 1); t += blockDim.x) {
+        const int i = 2 * t - (t & (j - 1));
+        const int ixj = i + j;
+        const unsigned long long a = s[i], b = s[ixj];
+        const bool up = (i & k) == 0;
+        if ((a > b) == up) {
+          s[i] = b;
+          s[ixj] = a;
+        }
+      }
+      __syncthreads();
+    }
+    for (int seg = wid * 64; seg < np; seg += nw * 64) {
+      unsigned long long v[2] = {s[seg + lane], s[seg + 32 + lane]};
+      seg_bitonic_low(v, seg, k, 32, lane);
+      s[seg + lane] = v[0];
+      s[seg + 32 + lane] = v[1];
+    }
+    __syncthreads();
+  }
+}
+
 // Register bitonic sort of 32*K 64-bit keys held by a warp, element
 // i = 32 r + lane in v[r]: partners at distance j < 32 are exchanged with
 // shuffles, larger distances are register swaps.  Ascending.
@@ -500,32 +562,39 @@ __device__ __forceinline__ void big_sort_body(
   const uint32_t nb = *(volatile uint32_t*)&sc->num_big;
   if (nb == 0) return;
   if (blockIdx.x == 0) {
-    // exclusive prefixes of sizes and chunk counts (list order is arbitrary;
-    // it only decides which CTA works on what)
-    uint32_t* tot = reinterpret_cast<uint32_t*>(s);
+    // exclusive prefixes over the big-tile list (its order is arbitrary; it
+    // only decides which CTA works on what): chunks of every big tile, and
+    // elements of the tiles that need merging (more than one chunk)
+    uint32_t* wsum = reinterpret_cast<uint32_t*>(s);  // [2][32] warp totals
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (threadIdx.x == 0) carry[0] = carry[1] = 0;
     __syncthreads();
     for (uint32_t b0 = 0; b0 < nb; b0 += blockDim.x) {
-      uint32_t j = b0 + threadIdx.x;
+      const uint32_t j = b0 + threadIdx.x;
       uint32_t sz = 0, ch = 0;
       if (j < nb) {
-        uint32_t t = big_tiles[j];
-        sz = ranges[t + 1] - ranges[t];
-        ch = (sz + kBigChunk - 1) / kBigChunk;
+        const uint32_t t = big_tiles[j];
+        const uint32_t n = ranges[t + 1] - ranges[t];
+        ch = (n + kBigChunk - 1) / kBigChunk;
+        sz = ch > 1 ? n : 0u;
       }
-      tot[threadIdx.x] = sz;
-      tot[blockDim.x + threadIdx.x] = ch;
+      uint32_t xs = sz, xc = ch;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t ys = __shfl_up_sync(0xffffffffu, xs, o), yc = __shfl_up_sync(0xffffffffu, xc, o);
+        if (lane >= o) { xs += ys; xc += yc; }
+      }
+      if (lane == 31) { wsum[wid] = xs; wsum[32 + wid] = xc; }
       __syncthreads();
-      if (threadIdx.x == 0) {  // serial per block of tiles: big tiles are few
-        uint32_t a = carry[0], c = carry[1];
-        for (uint32_t k = 0; k < blockDim.x && b0 + k < nb; ++k) {
-          big_elem[b0 + k] = a;
-          big_chunk[b0 + k] = c;
-          a += tot[k];
-          c += tot[blockDim.x + k];
-        }
-        carry[0] = a;
-        carry[1] = c;
+      uint32_t ps = carry[0], pc = carry[1];
+      for (int w = 0; w < wid; ++w) { ps += wsum[w]; pc += wsum[32 + w]; }
+      if (j < nb) {
+        big_elem[j] = ps + xs - sz;
+        big_chunk[j] = pc + xc - ch;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int w = 0; w < nw; ++w) { carry[0] += wsum[w]; carry[1] += wsum[32 + w]; }
       }
       __syncthreads();
     }
@@ -538,49 +607,58 @@ __device__ __forceinline__ void big_sort_body(
   grid.sync();
   const uint32_t total_chunks = big_chunk[nb], total = big_elem[nb], maxn = sc->max_big;
   for (uint32_t gch = blockIdx.x; gch < total_chunks; gch += gridDim.x) {
-    uint32_t j = upper_bound_u32(big_chunk, nb, gch) - 1;
-    uint32_t t = big_tiles[j];
-    uint32_t c = gch - big_chunk[j];
-    uint32_t begin = ranges[t] + c * kBigChunk;
-    uint32_t n = min((uint32_t)kBigChunk, ranges[t + 1] - begin);
+    const uint32_t j = upper_bound_u32(big_chunk, nb, gch) - 1;
+    const uint32_t t = big_tiles[j];
+    const uint32_t c = gch - big_chunk[j];
+    const uint32_t tn = ranges[t + 1] - ranges[t];
+    const uint32_t begin = ranges[t] + c * kBigChunk;
+    const uint32_t n = min((uint32_t)kBigChunk, ranges[t + 1] - begin);
     int np = 64;  // sort network of the next power of two, not the full chunk
     while (np < (int)n) np <<= 1;
     for (int k = threadIdx.x; k < np; k += blockDim.x) s[k] = k < (int)n ? entries[begin + k] : ~0ull;
     __syncthreads();
-    block_bitonic(s, np);
-    for (int k = threadIdx.x; k < (int)n; k += blockDim.x) entries[begin + k] = s[k];
+    block_bitonic_fast(s, np);
+    if (tn <= (uint32_t)kBigChunk) {  // one chunk = the whole tile: final order
+      for (int k = threadIdx.x; k < (int)n; k += blockDim.x) sorted_idx[begin + k] = (uint32_t)s[k];
+    } else {
+      for (int k = threadIdx.x; k < (int)n; k += blockDim.x) entries[begin + k] = s[k];
+    }
     __syncthreads();
   }
-  grid.sync();
-  unsigned long long* src = entries;
-  unsigned long long* dst = tmp;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t L = kBigChunk; L < maxn; L <<= 1) {
+  if (total > 0) {  // tiles over one chunk: pairwise merges of the sorted runs
+    grid.sync();
+    unsigned long long* src = entries;
+    unsigned long long* dst = tmp;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t L = kBigChunk; L < maxn; L <<= 1) {
+      for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+        uint32_t j = upper_bound_u32(big_elem, nb, e) - 1;
+        while (j + 1 < nb && big_elem[j + 1] == big_elem[j]) ++j;  // skip single-chunk tiles
+        uint32_t t = big_tiles[j];
+        uint32_t begin = ranges[t], n = ranges[t + 1] - begin;
+        uint32_t pos = e - big_elem[j];
+        uint32_t r = pos / L, run0 = r * L, p0 = (r ^ 1u) * L;
+        unsigned long long key = src[begin + pos];
+        uint32_t out = pos;
+        if (p0 < n) {
+          uint32_t p1 = min(p0 + L, n);
+          uint32_t rank = lower_bound_u64(src + begin + p0, p1 - p0, key);
+          out = min(run0, p0) + (pos - run0) + rank;
+        }
+        dst[begin + out] = key;
+      }
+      grid.sync();
+      unsigned long long* sw = src;
+      src = dst;
+      dst = sw;
+    }
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
       uint32_t j = upper_bound_u32(big_elem, nb, e) - 1;
-      uint32_t t = big_tiles[j];
-      uint32_t begin = ranges[t], n = ranges[t + 1] - begin;
+      while (j + 1 < nb && big_elem[j + 1] == big_elem[j]) ++j;
+      uint32_t begin = ranges[big_tiles[j]];
       uint32_t pos = e - big_elem[j];
-      uint32_t r = pos / L, run0 = r * L, p0 = (r ^ 1u) * L;
-      unsigned long long key = src[begin + pos];
-      uint32_t out = pos;
-      if (p0 < n) {
-        uint32_t p1 = min(p0 + L, n);
-        uint32_t rank = lower_bound_u64(src + begin + p0, p1 - p0, key);
-        out = min(run0, p0) + (pos - run0) + rank;
-      }
-      dst[begin + out] = key;
+      sorted_idx[begin + pos] = (uint32_t)src[begin + pos];
     }
-    grid.sync();
-    unsigned long long* sw = src;
-    src = dst;
-    dst = sw;
-  }
-  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    uint32_t j = upper_bound_u32(big_elem, nb, e) - 1;
-    uint32_t begin = ranges[big_tiles[j]];
-    uint32_t pos = e - big_elem[j];
-    sorted_idx[begin + pos] = (uint32_t)src[begin + pos];
   }
   grid.sync();  // everybody has read the big-tile counters: zero them for the next call
   if (blockIdx.x == 0 && threadIdx.x == 0) {
