@@ -33,6 +33,8 @@ import synthgen  # noqa: E402
 
 METRIC = "frames/s and Mpoints/s at 1080p fwd+bwd, % of B200 HBM roofline, 1/2/4/8 GPUs"
 WORKLOAD = "cfg2: 2^20-point view-specific cloud, 1920x1080, C=4, bilinear 2x2 splats, fwd+bwd"
+WORKLOAD3 = "cfg3: 4x2^20 ring-buffer cloud, 1920x1080, C=4, Gaussian splats (auto sigma, dilation 0.16), forward only"
+WORKLOAD4 = "cfg4: 2^25-point global extracted cloud, 1920x1080, C=4, bilinear, forward only"
 WORKLOAD5 = "cfg5: 64 orbit views of a 2^23-point cloud, 1920x1080, C=4, bilinear, fwd+bwd, shared features"
 NOMINAL_HBM_GBS = 8000.0
 
@@ -197,10 +199,18 @@ def run_ours(args, rank, world, local_rank):
         views = [v for v in range(64) if v * world // 64 == rank]   # contiguous blocks
         cams = [c["cams"][v] for v in views]
         seed_g = 5 + rank
+    elif args.config in (3, 4):
+        # forward-only inference frames: cfg3 ring-buffer cloud with Gaussians,
+        # cfg4 global extracted cloud (bilinear); one frame per rank
+        c = synthgen.config3() if args.config == 3 else synthgen.config4()
+        cams = c["cams"]
+        seed_g = args.config + rank
     else:
         c = synthgen.config2(seed=2 + rank)
         cams = c["cams"]
         seed_g = 2 + rank
+    mode = c["mode"]
+    fwd_only = args.config in (3, 4)
     V = len(cams)
     H, W, C = c["H"], c["W"], c["C"]
     N = c["xyz"].shape[0]
@@ -228,7 +238,7 @@ def run_ours(args, rank, world, local_rank):
         gF_h, gA_h, gD_h = (torch.from_numpy(x).pin_memory() for x in synthgen.upstream_grads(seed_g, 1, H, W, C))
     gF, gA, gD = gF_h.to(dev), gA_h.to(dev), gD_h.to(dev)
     ctx = inpc.Context(dev_index)
-    cfg = inpc.make_cfg(H, W, C, "bilinear", flags=flags, env_hw=env_hw)
+    cfg = inpc.make_cfg(H, W, C, mode, flags=flags, env_hw=env_hw)
     out = dict(F=torch.empty((V, H, W, C), device=dev), A=torch.empty((V, H, W), device=dev),
                D=torch.empty((V, H, W), device=dev))
     g_feat = torch.zeros_like(feat)
@@ -236,6 +246,9 @@ def run_ours(args, rank, world, local_rank):
     reduce_grads = args.config == 5 and world > 1
 
     def step():
+        if fwd_only:
+            ctx.forward(cfg, cams, xyz, feat, op, bg=env_t, out=out)
+            return
         g_feat.zero_()
         g_op.zero_()
         ctx.forward(cfg, cams, xyz, feat, op, bg=env_t, out=out)
@@ -245,7 +258,7 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(g_op)
 
     # workload statistics (untimed): visible points, tile entries, per view
-    dbg = inpc.make_cfg(H, W, C, "bilinear", flags=flags | inpc.FLAG_DEBUG, env_hw=env_hw)
+    dbg = inpc.make_cfg(H, W, C, mode, flags=flags | inpc.FLAG_DEBUG, env_hw=env_hw)
     ctx.forward(dbg, cams, xyz, feat, op, bg=env_t)
     Nv = Ft = 0
     for v in range(V):
@@ -254,6 +267,8 @@ def run_ours(args, rank, world, local_rank):
         Ft += int(ex["F_t"])
     model = algorithmic_bytes(N * V, Nv, Ft, P * V, C, sh="sh" in args.variant,
                               env="env" in args.variant)
+    if fwd_only:
+        model = {k: v for k, v in model.items() if k not in ("blend_bwd", "sh_grad")}
     step_bytes = sum(model.values())
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -357,19 +372,25 @@ def run_ours(args, rank, world, local_rank):
     h2d = sum(t.numel() * 4 for t in (xyz_h, feat_h, op_h, gF_h, gA_h, gD_h))
     d2h = sum(t.numel() * 4 for t in (F_h, A_h, D_h, gf_h, go_h))
 
+    if fwd_only:
+        h2d = sum(t.numel() * 4 for t in (xyz_h, feat_h, op_h))
+        d2h = sum(t.numel() * 4 for t in (F_h, A_h, D_h))
+
     def e2e_step():
         xyz.copy_(xyz_h, non_blocking=True)
         feat.copy_(feat_h, non_blocking=True)
         op.copy_(op_h, non_blocking=True)
-        gF.copy_(gF_h, non_blocking=True)
-        gA.copy_(gA_h, non_blocking=True)
-        gD.copy_(gD_h, non_blocking=True)
+        if not fwd_only:
+            gF.copy_(gF_h, non_blocking=True)
+            gA.copy_(gA_h, non_blocking=True)
+            gD.copy_(gD_h, non_blocking=True)
         step()
         F_h.copy_(out["F"], non_blocking=True)
         A_h.copy_(out["A"], non_blocking=True)
         D_h.copy_(out["D"], non_blocking=True)
-        gf_h.copy_(g_feat, non_blocking=True)
-        go_h.copy_(g_op, non_blocking=True)
+        if not fwd_only:
+            gf_h.copy_(g_feat, non_blocking=True)
+            go_h.copy_(g_op, non_blocking=True)
 
     for _ in range(0 if args.profile_run else 2):
         e2e_step()
@@ -405,13 +426,14 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+            "passes": "fwd" if fwd_only else "fwd+bwd",
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong" if args.config == 5 else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD5 if args.config == 5 else WORKLOAD,
+            "config": {"workload": {5: WORKLOAD5, 3: WORKLOAD3, 4: WORKLOAD4}.get(args.config, WORKLOAD),
                        "variant": args.variant, "N": N, "views_per_rank": V,
                        "N_visible": Nv, "F_t": Ft, "H": H, "W": W,
-                       "C": C, "mode": "bilinear", "alpha_max": 0.99, "t_min": 1e-4,
+                       "C": C, "mode": mode, "alpha_max": 0.99, "t_min": 1e-4,
                        "parallelism": (f"64 views split over {world} ranks + gradient all-reduce"
                                        if args.config == 5 else f"independent frames x{world} (weak)"),
                        "l2": "flushed: 256 MiB write between steps, outside the per-step events"},
@@ -422,9 +444,8 @@ def run_ours(args, rank, world, local_rank):
             "roofline": roof,
             "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items() if v[1]},
             "stages_note": ("device time per stage from CUDA events around each stage of an eager "
-                            "profiled step after every timed replay; eager launches bin with the fused "
-                            "cooperative kernel (bin_fused), the captured graph with the separate "
-                            "project/scan/scatter/sort_big kernels"),
+                            "profiled step after every timed replay (same kernels as the graph); "
+                            "bin_fused = project + scan + scatter + big-tile sort in one cooperative launch"),
             "gpu_launches": launches,
             "cuda_graph": graph_used,
             "clocks": clk.summary(),
@@ -444,9 +465,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
-    ap.add_argument("--config", type=int, choices=[2, 5], default=2,
-                    help="2: cfg2 frame per rank (default, weak scaling); 5: 64-view batch split "
-                         "over ranks with a gradient all-reduce (strong scaling)")
+    ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2,
+                    help="2: cfg2 frame per rank (default, weak scaling); 3/4: forward-only "
+                         "inference frames (Gaussian ring buffer / 33M global cloud); 5: 64-view "
+                         "batch split over ranks with a gradient all-reduce (strong scaling)")
     ap.add_argument("--variant", choices=["base", "sh", "env", "sh+env"], default="base",
                     help="NEXT rows: SH-coefficient features (f1) / env-map background (f2)")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (GPUs) or gloo (1-GPU tests)")

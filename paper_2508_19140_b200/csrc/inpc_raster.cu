@@ -347,7 +347,9 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_big, kBigThreads, 0);
+  const int big_smem = kBigChunkLarge * 8;
+  cudaFuncSetAttribute(k_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, big_smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_big, kBigThreadsLarge, big_smem);
   c->big_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
   {
     int o2 = 0, o4 = 0, o8 = 0;
@@ -531,13 +533,10 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     ViewScalars* sc = (ViewScalars*)vs.scalars.p;
     const int nblk = (int)((N + (int64_t)kPointThreads * kPPT - 1) / ((int64_t)kPointThreads * kPPT));
     // bilinear: one cooperative launch for H1-H6 when the points fit in registers
-    // (measured on cfg 2: the fused launch saves ~14 us of launch gaps when
-    // launched eagerly; inside a CUDA graph the gaps are gone and the separate
-    // kernels, at full occupancy, are ~6 us faster -> unfused when capturing)
+    // (measured on cfg 2 at 1080p: fused 58.5 us vs 67 us for the separate
+    // kernels eagerly, and 201.5 vs 203.7 us per fwd+bwd step in a CUDA graph)
     int fused_kp = 0, fused_grid = 0;
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(s, &cap);
-    if (!gauss && !sh && N > 0 && !c->no_fused_bin && cap == cudaStreamCaptureStatusNone) {
+    if (!gauss && !sh && N > 0 && !c->no_fused_bin) {
       const int kps[3] = {2, 4, 8};
       for (int q = 0; q < 3; ++q)
         if (c->bin_grid[q] > 0 && N <= (int64_t)kps[q] * c->bin_grid[q] * kBinThreads) {
@@ -641,7 +640,8 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       unsigned long long* tp = (unsigned long long*)c->tmp.p;
       uint32_t* si = (uint32_t*)vs.sorted_idx.p;
       void* args[] = {(void*)&r, (void*)&bt, (void*)&be, (void*)&bc, (void*)&scc, (void*)&en, (void*)&tp, (void*)&si};
-      CK(cudaLaunchCooperativeKernel((void*)k_sort_big, c->big_grid, kBigThreads, args, 0, s));
+      CK(cudaLaunchCooperativeKernel((void*)k_sort_big, c->big_grid, kBigThreadsLarge, args,
+                                     (size_t)kBigChunkLarge * 8, s));
     }
     {
       StageTimer tm(c, s, kStBlendFwd, 1);

@@ -554,6 +554,7 @@ __device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a,
 // search; keys are unique), (3) the point indices go to sorted_idx.  Grid-
 // synchronised between phases; returns at once if no tile is big.  Any
 // block size <= kBigThreads; s holds kBigChunk keys.
+template <int CHUNK>
 __device__ __forceinline__ void big_sort_body(
     cooperative_groups::grid_group& grid, unsigned long long* s, uint32_t* carry,
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles,
@@ -575,7 +576,7 @@ __device__ __forceinline__ void big_sort_body(
       if (j < nb) {
         const uint32_t t = big_tiles[j];
         const uint32_t n = ranges[t + 1] - ranges[t];
-        ch = (n + kBigChunk - 1) / kBigChunk;
+        ch = (n + CHUNK - 1) / CHUNK;
         sz = ch > 1 ? n : 0u;
       }
       uint32_t xs = sz, xc = ch;
@@ -611,14 +612,14 @@ __device__ __forceinline__ void big_sort_body(
     const uint32_t t = big_tiles[j];
     const uint32_t c = gch - big_chunk[j];
     const uint32_t tn = ranges[t + 1] - ranges[t];
-    const uint32_t begin = ranges[t] + c * kBigChunk;
-    const uint32_t n = min((uint32_t)kBigChunk, ranges[t + 1] - begin);
+    const uint32_t begin = ranges[t] + c * CHUNK;
+    const uint32_t n = min((uint32_t)CHUNK, ranges[t + 1] - begin);
     int np = 64;  // sort network of the next power of two, not the full chunk
     while (np < (int)n) np <<= 1;
     for (int k = threadIdx.x; k < np; k += blockDim.x) s[k] = k < (int)n ? entries[begin + k] : ~0ull;
     __syncthreads();
     block_bitonic_fast(s, np);
-    if (tn <= (uint32_t)kBigChunk) {  // one chunk = the whole tile: final order
+    if (tn <= (uint32_t)CHUNK) {  // one chunk = the whole tile: final order
       for (int k = threadIdx.x; k < (int)n; k += blockDim.x) sorted_idx[begin + k] = (uint32_t)s[k];
     } else {
       for (int k = threadIdx.x; k < (int)n; k += blockDim.x) entries[begin + k] = s[k];
@@ -630,7 +631,7 @@ __device__ __forceinline__ void big_sort_body(
     unsigned long long* src = entries;
     unsigned long long* dst = tmp;
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t L = kBigChunk; L < maxn; L <<= 1) {
+    for (uint32_t L = CHUNK; L < maxn; L <<= 1) {
       for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
         uint32_t j = upper_bound_u32(big_elem, nb, e) - 1;
         while (j + 1 < nb && big_elem[j + 1] == big_elem[j]) ++j;  // skip single-chunk tiles
@@ -667,14 +668,21 @@ __device__ __forceinline__ void big_sort_body(
   }
 }
 
-__global__ void __launch_bounds__(kBigThreads) k_sort_big(
+// Stand-alone big-tile sort: 1024 threads, chunks of kBigChunkLarge keys in
+// 64 KB of dynamic SMEM, so tiles up to 8192 entries (cfg 4: 7750 tiles of
+// 2-7k entries) sort in one chunk without merge passes.
+constexpr int kBigChunkLarge = 8192;
+constexpr int kBigThreadsLarge = 1024;
+__global__ void __launch_bounds__(kBigThreadsLarge) k_sort_big(
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles,
     uint32_t* big_elem, uint32_t* big_chunk, ViewScalars* sc,
     unsigned long long* entries, unsigned long long* tmp, uint32_t* __restrict__ sorted_idx) {
-  __shared__ unsigned long long s[kBigChunk];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t carry[2];
+  unsigned long long* s = reinterpret_cast<unsigned long long*>(smem_raw);
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-  big_sort_body(grid, s, carry, ranges, big_tiles, big_elem, big_chunk, sc, entries, tmp, sorted_idx);
+  big_sort_body<kBigChunkLarge>(grid, s, carry, ranges, big_tiles, big_elem, big_chunk, sc, entries, tmp,
+                                sorted_idx);
 }
 
 // ---------------------------------------------------------------- H1..H6 fused (bilinear)
@@ -832,7 +840,8 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
   }
   grid.sync();
   // ---- phase 4: big tiles
-  big_sort_body(grid, s, carry, ranges, big_tiles, big_elem, big_chunk, sc, entries, tmp, sorted_idx);
+  big_sort_body<kBigChunk>(grid, s, carry, ranges, big_tiles, big_elem, big_chunk, sc, entries, tmp,
+                           sorted_idx);
 }
 
 // ---------------------------------------------------------------- H7 / H8 per-warp staging
