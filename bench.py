@@ -376,31 +376,67 @@ def run_ours(args, rank, world, local_rank):
         h2d = sum(t.numel() * 4 for t in (xyz_h, feat_h, op_h))
         d2h = sum(t.numel() * 4 for t in (F_h, A_h, D_h))
 
-    def e2e_step():
-        xyz.copy_(xyz_h, non_blocking=True)
-        feat.copy_(feat_h, non_blocking=True)
-        op.copy_(op_h, non_blocking=True)
-        if not fwd_only:
-            gF.copy_(gF_h, non_blocking=True)
-            gA.copy_(gA_h, non_blocking=True)
-            gD.copy_(gD_h, non_blocking=True)
-        step()
-        F_h.copy_(out["F"], non_blocking=True)
-        A_h.copy_(out["A"], non_blocking=True)
-        D_h.copy_(out["D"], non_blocking=True)
-        if not fwd_only:
-            gf_h.copy_(g_feat, non_blocking=True)
-            go_h.copy_(g_op, non_blocking=True)
+    # two device buffer sets so that step k+1's H2D and step k-1's D2H overlap
+    # step k's kernels (three streams; a serving / training input pipeline)
+    sets = [dict(xyz=xyz, feat=feat, op=op, gF=gF, gA=gA, gD=gD, out=out, g_feat=g_feat, g_op=g_op)]
+    if not args.profile_run:
+        sets.append({k: (v.clone() if torch.is_tensor(v) else {kk: vv.clone() for kk, vv in v.items()})
+                     for k, v in sets[0].items()})
+    s_comp = torch.cuda.current_stream()
+    s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in sets]
+    ev_done = [torch.cuda.Event() for _ in sets]
+    ev_read = [torch.cuda.Event() for _ in sets]
+    for e in ev_done + ev_read:
+        e.record(s_comp)
 
-    for _ in range(0 if args.profile_run else 2):
-        e2e_step()
-    n_e2e = 1 if args.profile_run else max(3, min(args.steps, 20))
+    def e2e_step(k):
+        b = k % len(sets)
+        S = sets[b]
+        with torch.cuda.stream(s_h2d):
+            s_h2d.wait_event(ev_done[b])          # set b's previous compute has read its inputs
+            S["xyz"].copy_(xyz_h, non_blocking=True)
+            S["feat"].copy_(feat_h, non_blocking=True)
+            S["op"].copy_(op_h, non_blocking=True)
+            if not fwd_only:
+                S["gF"].copy_(gF_h, non_blocking=True)
+                S["gA"].copy_(gA_h, non_blocking=True)
+                S["gD"].copy_(gD_h, non_blocking=True)
+            ev_in[b].record(s_h2d)
+        s_comp.wait_event(ev_in[b])
+        s_comp.wait_event(ev_read[b])             # set b's previous outputs were copied out
+        if fwd_only:
+            ctx.forward(cfg, cams, S["xyz"], S["feat"], S["op"], bg=env_t, out=S["out"])
+        else:
+            S["g_feat"].zero_()
+            S["g_op"].zero_()
+            ctx.forward(cfg, cams, S["xyz"], S["feat"], S["op"], bg=env_t, out=S["out"])
+            ctx.backward(cfg, cams, S["xyz"], S["feat"], S["op"], S["gF"], S["gA"], S["gD"], bg=env_t,
+                         g_feat=S["g_feat"], g_opacity=S["g_op"])
+            if reduce_grads:
+                dist.all_reduce(S["g_feat"])
+                dist.all_reduce(S["g_op"])
+        ev_done[b].record(s_comp)
+        with torch.cuda.stream(s_d2h):
+            s_d2h.wait_event(ev_done[b])
+            F_h.copy_(S["out"]["F"], non_blocking=True)
+            A_h.copy_(S["out"]["A"], non_blocking=True)
+            D_h.copy_(S["out"]["D"], non_blocking=True)
+            if not fwd_only:
+                gf_h.copy_(S["g_feat"], non_blocking=True)
+                go_h.copy_(S["g_op"], non_blocking=True)
+            ev_read[b].record(s_d2h)
+
+    for k in range(0 if args.profile_run else 2):
+        e2e_step(k)
+    n_e2e = 1 if args.profile_run else max(4, min(args.steps, 20))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(n_e2e):
-        e2e_step()
-    e1.record()
+    e0.record(s_h2d)
+    for k in range(n_e2e):
+        e2e_step(k)
+    s_d2h.wait_stream(s_comp)
+    e1.record(s_d2h)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / n_e2e
     if world > 1:
@@ -450,7 +486,10 @@ def run_ours(args, rank, world, local_rank):
             "cuda_graph": graph_used,
             "clocks": clk.summary(),
             "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                    "note": ("public API with pinned host buffers; every step copies its inputs "
+                             "(cloud + upstream gradients) in and its image + gradients out; H2D of "
+                             "step k+1 and D2H of step k-1 overlap step k (two device buffer sets)")},
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -17,7 +17,7 @@ out_dir = os.path.join(ROOT, "profiles")
 os.makedirs(out_dir, exist_ok=True)
 STAGE = {"k_project_count": "project_count", "k_scan_tiles": "scan_tiles", "k_scatter": "scatter",
          "k_scatter_slots": "scatter", "k_sort_big": "sort_big", "k_blend_fwd": "blend_fwd",
-         "k_blend_bwd": "blend_bwd"}
+         "k_blend_bwd": "blend_bwd", "k_bin_bilinear": "bin_fused", "k_sh_grad": "sh_grad"}
 raw = list(csv.reader(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
                                      capture_output=True, text=True).stdout.splitlines()))
 h, units = raw[0], raw[1]
