@@ -38,6 +38,7 @@
 #ifndef INPC_RASTER_H
 #define INPC_RASTER_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #if defined(__GNUC__)
@@ -110,11 +111,22 @@ typedef struct {
 
 typedef struct inpc_ctx inpc_ctx;
 
+/* Device-memory allocator of the caller (e.g. PyTorch's caching allocator):
+ * alloc returns `bytes` of device memory usable on `stream` (NULL = out of
+ * memory); free releases a pointer alloc returned (stream NULL at context
+ * destruction).  Without one the context uses cudaMalloc / cudaFree. */
+typedef void* (*inpc_alloc_fn)(size_t bytes, int device, void* stream, void* user);
+typedef void (*inpc_free_fn)(void* ptr, size_t bytes, int device, void* stream, void* user);
+
 /* Create a context on CUDA device `device` (the caller's current device is
  * restored).  *out receives the handle. */
 INPC_API int inpc_ctx_create(inpc_ctx** out, int device);
-/* Free the context's arena and saved state (synchronises its last stream). */
+/* Free the context's arena and saved state (synchronises the device). */
 INPC_API int inpc_ctx_destroy(inpc_ctx* ctx);
+/* Route the context's scratch arena and saved state through a caller
+ * allocator (both functions, or both NULL for cudaMalloc).  Releases the
+ * current arena (and the saved forward state) first. */
+INPC_API int inpc_ctx_set_allocator(inpc_ctx* ctx, inpc_alloc_fn alloc, inpc_free_fn free_fn, void* user);
 
 /* Forward raster of V views of one point cloud.
  *   cams   [V] host cameras

@@ -32,8 +32,13 @@ TILE = 8
 
 EXPORTS = ("inpc_ctx_create", "inpc_ctx_destroy", "inpc_rasterize_fwd", "inpc_rasterize_bwd",
            "inpc_debug_export", "inpc_ctx_set_profiling", "inpc_ctx_stage_times",
-           "inpc_ctx_forget_events",
+           "inpc_ctx_forget_events", "inpc_ctx_set_allocator",
            "inpc_stage_name", "inpc_status_string", "inpc_version")
+
+
+# inpc_alloc_fn / inpc_free_fn (include/inpc_raster.h)
+ALLOC_FN = ct.CFUNCTYPE(ct.c_void_p, ct.c_size_t, ct.c_int, ct.c_void_p, ct.c_void_p)
+FREE_FN = ct.CFUNCTYPE(None, ct.c_void_p, ct.c_size_t, ct.c_int, ct.c_void_p, ct.c_void_p)
 
 
 class RasterError(RuntimeError):
@@ -73,6 +78,7 @@ def _load():
     lib.inpc_ctx_stage_times.argtypes = [P, ct.POINTER(ct.c_float), ct.POINTER(i64), i32,
                                          ct.POINTER(i32), ct.c_int]
     lib.inpc_ctx_forget_events.argtypes = [P]
+    lib.inpc_ctx_set_allocator.argtypes = [P, ALLOC_FN, FREE_FN, P]
     lib.inpc_stage_name.argtypes = [i32]
     lib.inpc_stage_name.restype = ct.c_char_p
     lib.inpc_status_string.argtypes = [ct.c_int]
@@ -161,13 +167,29 @@ def _strides(cfg, N, feat, bg):
 class Context:
     """Owns an inpc_ctx (scratch arena + the state saved by forward)."""
 
-    def __init__(self, device=None):
+    def __init__(self, device=None, torch_allocator=True):
+        """torch_allocator: the library's scratch arena and saved state come
+        from PyTorch's caching allocator (inpc_ctx_set_allocator) instead of
+        cudaMalloc."""
         import torch
         dev = torch.cuda.current_device() if device is None else int(device)
         self.device = dev
         h = ct.c_void_p()
         _check(lib.inpc_ctx_create(ct.byref(h), dev))
         self._h = h
+        self._cb = None
+        if torch_allocator:
+            def _alloc(nbytes, device, stream, user):
+                try:
+                    return torch.cuda.caching_allocator_alloc(int(nbytes), device, stream or 0)
+                except Exception:       # out of memory -> NULL -> INPC_OOM
+                    return None
+
+            def _free(ptr, nbytes, device, stream, user):
+                torch.cuda.caching_allocator_delete(ptr)
+
+            self._cb = (ALLOC_FN(_alloc), FREE_FN(_free))
+            _check(lib.inpc_ctx_set_allocator(self._h, self._cb[0], self._cb[1], None))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -20,6 +20,17 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// Optional caller allocator (inpc_ctx_set_allocator), made current for the
+// duration of an API call by AllocScope.
+struct Allocator {
+  inpc_alloc_fn alloc = nullptr;
+  inpc_free_fn free = nullptr;
+  void* user = nullptr;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+};
+thread_local const Allocator* g_alloc = nullptr;
+
 struct Buf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -78,7 +89,10 @@ struct inpc_ctx {
   int64_t pending_launches[kNumStages] = {};  // kernel launches behind the pending event pairs
   cudaStream_t last_stream = nullptr;
   uint32_t* host_scalars = nullptr;  // pinned
+  Allocator allocator;               // caller allocator (or cudaMalloc when unset)
 };
+
+
 
 namespace {
 
@@ -115,11 +129,18 @@ int ensure(Buf& b, size_t bytes, cudaStream_t s, bool* fresh = nullptr) {
   size_t nb = bytes < 256 ? 256 : bytes + bytes / 4;
   if (b.p) {
     cudaStreamSynchronize(s);
-    cudaFree(b.p);
+    if (g_alloc && g_alloc->free) g_alloc->free(b.p, b.bytes, g_alloc->device, (void*)s, g_alloc->user);
+    else cudaFree(b.p);
     b.p = nullptr;
     b.bytes = 0;
   }
-  if (cudaMalloc(&b.p, nb) != cudaSuccess) {
+  if (g_alloc && g_alloc->alloc) {
+    b.p = g_alloc->alloc(nb, g_alloc->device, (void*)s, g_alloc->user);
+    if (!b.p) {
+      g_last_error = "caller allocator returned NULL";
+      return INPC_OOM;
+    }
+  } else if (cudaMalloc(&b.p, nb) != cudaSuccess) {
     cudaGetLastError();
     g_last_error = "cudaMalloc failed";
     return INPC_OOM;
@@ -129,9 +150,30 @@ int ensure(Buf& b, size_t bytes, cudaStream_t s, bool* fresh = nullptr) {
 }
 
 void free_buf(Buf& b) {
-  if (b.p) cudaFree(b.p);
+  if (b.p) {
+    if (g_alloc && g_alloc->free) g_alloc->free(b.p, b.bytes, g_alloc->device, nullptr, g_alloc->user);
+    else cudaFree(b.p);
+  }
   b.p = nullptr;
   b.bytes = 0;
+}
+
+struct AllocScope {
+  const Allocator* prev;
+  explicit AllocScope(inpc_ctx* c) : prev(g_alloc) { g_alloc = c->allocator.alloc ? &c->allocator : nullptr; }
+  ~AllocScope() { g_alloc = prev; }
+};
+
+void release_all(inpc_ctx* c) {
+  for (Buf* b : {&c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots,
+                 &c->agg, &c->g_eval, &c->tmp, &c->overflow})
+    free_buf(*b);
+  for (auto& v : c->views)
+    for (Buf* b : {&v.ranges, &v.sorted_idx, &v.T_final, &v.last, &v.dbg_key, &v.dbg_tiles, &v.scalars,
+                   &v.rec, &v.feat_eval})
+      free_buf(*b);
+  c->views.clear();
+  c->have_state = false;
 }
 
 bool is_device_ptr(const void* p) {
@@ -377,13 +419,10 @@ int inpc_ctx_destroy(inpc_ctx* c) {
   if (!c) return INPC_INVALID_ARG;
   DeviceGuard dg(c->device);
   cudaDeviceSynchronize();
-  for (Buf* b : {&c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots, &c->agg, &c->g_eval,
-                 &c->tmp, &c->overflow})
-    free_buf(*b);
-  for (auto& v : c->views)
-    for (Buf* b : {&v.ranges, &v.sorted_idx, &v.T_final, &v.last, &v.dbg_key, &v.dbg_tiles, &v.scalars,
-                   &v.rec, &v.feat_eval})
-      free_buf(*b);
+  {
+    AllocScope as(c);
+    release_all(c);
+  }
   for (auto& e : c->pending) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -391,6 +430,21 @@ int inpc_ctx_destroy(inpc_ctx* c) {
   for (auto e : c->pool) cudaEventDestroy(e);
   if (c->host_scalars) cudaFreeHost(c->host_scalars);
   delete c;
+  return INPC_OK;
+}
+
+int inpc_ctx_set_allocator(inpc_ctx* c, inpc_alloc_fn alloc, inpc_free_fn free_fn, void* user) {
+  if (!c || (!alloc) != (!free_fn)) return INPC_INVALID_ARG;
+  DeviceGuard dg(c->device);
+  cudaDeviceSynchronize();
+  {
+    AllocScope as(c);  // the arena goes back to whoever allocated it
+    release_all(c);
+  }
+  c->allocator.alloc = alloc;
+  c->allocator.free = free_fn;
+  c->allocator.user = user;
+  c->allocator.device = c->device;
   return INPC_OK;
 }
 
@@ -475,6 +529,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   cudaStream_t s = (cudaStream_t)stream;
   c->last_stream = s;
   cudaGetLastError();
+  AllocScope alloc_scope(c);
 
   DevCam dc;
   DevCfg g;
@@ -719,6 +774,7 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   cudaStream_t s = (cudaStream_t)stream;
   c->last_stream = s;
   cudaGetLastError();
+  AllocScope alloc_scope(c);
   const int band_tiles = (g.ty1 - g.ty0) * g.tiles_x;
   const bool gauss = cfg->splat_mode == INPC_SPLAT_GAUSSIAN;
   const int cmax = cmax_for(cfg->C);

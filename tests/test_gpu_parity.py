@@ -351,3 +351,16 @@ def test_env_background_fwd_bwd(inpc, ctx):
     o = oracle.backward(cam, c["xyz"], c["feat"], c["opacity"], H, W, gF, gA, gD, bg=bg)
     check_grads(gf.cpu().numpy(), o["g_feat"])
     check_grads(go.cpu().numpy(), o["g_opacity"])
+
+
+def test_cudamalloc_and_torch_allocator_agree(inpc):
+    """The scratch arena from PyTorch's caching allocator (default) or from
+    cudaMalloc gives the same lists and images."""
+    c = synthgen.config1(seed=77)
+    a = inpc.Context(0, torch_allocator=True)
+    b = inpc.Context(0, torch_allocator=False)
+    _, _, ra = gpu_forward(inpc, a, c)
+    _, _, rb = gpu_forward(inpc, b, c)
+    for k in ("F", "A", "D", "sorted_idx", "tile_ranges", "nfrag"):
+        np.testing.assert_array_equal(ra[k], rb[k])
+    a.close(); b.close()
