@@ -364,3 +364,25 @@ def test_cudamalloc_and_torch_allocator_agree(inpc):
     for k in ("F", "A", "D", "sorted_idx", "tile_ranges", "nfrag"):
         np.testing.assert_array_equal(ra[k], rb[k])
     a.close(); b.close()
+
+
+def test_screen_bands_assemble_bit_exact(inpc, ctx):
+    """Sort-first sharding: each band rendered on its own with
+    cfg.tile_y_begin/end and assembled equals the unsharded frame bit for bit
+    (compositing is per pixel, so screen-space partitions are exact)."""
+    from paper_2508_19140_b200 import dist as pdist
+    c = synthgen.config2(N=1 << 16, H=200, W=264)
+    H, W = c["H"], c["W"]
+    xyz, feat, op = dev(c["xyz"]), dev(c["feat"]), dev(c["opacity"])
+    full = ctx.forward(inpc.make_cfg(H, W, 4), c["cams"], xyz, feat, op)
+    rows = (H + 7) // 8
+    for world in (2, 3, 5):
+        bands = pdist.band_split(np.arange(rows) % 7 + 1.0, world)
+        asm = torch.zeros_like(full["F"])
+        for b0, b1 in bands:
+            if b1 <= b0:
+                continue
+            o = ctx.forward(inpc.make_cfg(H, W, 4, band=(b0, b1)), c["cams"], xyz, feat, op)
+            asm[:, b0 * 8:min(b1 * 8, H)] = o["F"][:, b0 * 8:min(b1 * 8, H)]
+        torch.cuda.synchronize()
+        assert torch.equal(asm, full["F"])
