@@ -183,6 +183,59 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ GPU leg
+def run_sort_ab(args):
+    """NEXT f4: the paper's own sort comparison on B200, cfg 2:
+    the original single 64-bit sort of 4 copies per point vs this build's
+    tiled ordering (bucket scatter + per-tile register sorts)."""
+    import math
+
+    import torch
+
+    import paper_2508_19140_b200 as inpc
+    torch.cuda.set_device(0)
+    c = synthgen.config2()
+    H, W, C = c["H"], c["W"], c["C"]
+    N = c["xyz"].shape[0]
+    xyz, feat, op = (torch.from_numpy(c[k]).cuda() for k in ("xyz", "feat", "opacity"))
+    ctx = inpc.Context(0)
+    cfg = inpc.make_cfg(H, W, C)
+    for _ in range(3):
+        ctx.sort_single64(cfg, c["cams"][0], xyz, op)
+        ctx.forward(cfg, c["cams"], xyz, feat, op)
+    torch.cuda.synchronize()
+    ctx.stage_times(reset=True)
+    ctx.set_profiling(True)
+    reps = max(5, args.steps // 10)
+    F = 0
+    for _ in range(reps):
+        _, idx = ctx.sort_single64(cfg, c["cams"][0], xyz, op)
+        F = idx.numel()
+        ctx.forward(cfg, c["cams"], xyz, feat, op)
+    st = ctx.stage_times(reset=True)
+    ctx.set_profiling(False)
+    dbg = inpc.make_cfg(H, W, C, flags=inpc.FLAG_DEBUG)
+    ctx.forward(dbg, c["cams"], xyz, feat, op)
+    Ft = ctx.debug_export(0, H=H, W=W)["F_t"]
+    single_us = st["single_sort"][0] / reps * 1e3
+    bin_us = st["bin_fused"][0] / reps * 1e3
+    fwd_us = st["blend_fwd"][0] / reps * 1e3
+    pbits = (H * W - 1).bit_length()
+    line = {
+        "mode": "sort A/B (NEXT f4)", "workload": WORKLOAD,
+        "original_single_sort": {"us": single_us, "keys": 4 * N, "real_fragments": F,
+                                 "key_bits": 32 + pbits, "passes": math.ceil((32 + pbits) / 8),
+                                 "keys_per_s": 4 * N / (single_us * 1e-6),
+                                 "paper_model": "4 ceil((32+21)/8) n = 28n (P:162)"},
+        "tiled": {"bin_us": bin_us, "tile_entries": Ft, "entries_per_s": Ft / (bin_us * 1e-6),
+                  "blend_fwd_us_incl_tile_sorts": fwd_us,
+                  "paper_model": "4n depth + 2.54n tile = 6.54n (P:171-172); here 1 atomic bucket "
+                                 "scatter of 1.27n + per-tile sorts in registers inside blend_fwd"},
+        "speedup_bin_vs_single_sort": single_us / bin_us,
+    }
+    print(json.dumps(line), flush=True)
+    ctx.close()
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -549,6 +602,8 @@ def main():
     ap.add_argument("--variant", choices=["base", "sh", "env", "sh+env"], default="base",
                     help="NEXT rows: SH-coefficient features (f1) / env-map background (f2)")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (GPUs) or gloo (1-GPU tests)")
+    ap.add_argument("--sort-ab", action="store_true",
+                    help="NEXT f4: original single 64-bit sort vs the tiled ordering (one JSON line)")
     ap.add_argument("--profile-run", action="store_true",
                     help="for ncu: no clock ramp, no e2e leg, no CPU baseline")
     args = ap.parse_args()
@@ -558,6 +613,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.sort_ab:
+        run_sort_ab(args)
         return
     if world > 1:
         import torch

@@ -176,6 +176,20 @@ INPC_API int inpc_debug_export(inpc_ctx* ctx, int32_t view, uint32_t* depth_keys
                       uint32_t* tile_ranges, uint32_t* sorted_idx, int64_t sorted_cap,
                       int64_t* F_t_out, void* stream);
 
+/* NEXT f4 — the original INPC ordering as an A/B baseline (P:100,
+ * P:159-162): 4 fragment copies per point with 64-bit keys (pixel << 32 |
+ * depth bits), one stable device-wide LSD radix sort of 8-bit digits
+ * (ceil((32 + pixel bits) / 8) passes: 7 at 1080p), per-pixel ranges.
+ *   cam (host) one camera; xyz [N,3], opacity [N] (device)
+ *   pixel_ranges [H*W+1] u32 (device): pixel p's fragments are
+ *     sorted_idx[pixel_ranges[p] .. pixel_ranges[p+1]) in (depth, index) order
+ *   sorted_idx [sorted_cap] u32 (device) or NULL; F_out (host) = #fragments
+ * Bilinear only (INPC_UNSUPPORTED otherwise).  Synchronises the stream once
+ * (F readback).  The sort's device time is the "single_sort" profiling stage. */
+INPC_API int inpc_sort_single64(inpc_ctx* ctx, const inpc_raster_cfg* cfg, const inpc_camera* cam,
+                                const float* xyz, const float* opacity, int64_t N, uint32_t* pixel_ranges,
+                                uint32_t* sorted_idx, int64_t sorted_cap, int64_t* F_out, void* stream);
+
 /* Per-stage device timing (CUDA events around each stage; adds no sync to
  * the calls).  inpc_ctx_stage_times waits for the recorded events, adds
  * their elapsed milliseconds to per-stage accumulators and returns the

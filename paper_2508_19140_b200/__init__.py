@@ -32,7 +32,7 @@ TILE = 8
 
 EXPORTS = ("inpc_ctx_create", "inpc_ctx_destroy", "inpc_rasterize_fwd", "inpc_rasterize_bwd",
            "inpc_debug_export", "inpc_ctx_set_profiling", "inpc_ctx_stage_times",
-           "inpc_ctx_forget_events", "inpc_ctx_set_allocator",
+           "inpc_ctx_forget_events", "inpc_ctx_set_allocator", "inpc_sort_single64",
            "inpc_stage_name", "inpc_status_string", "inpc_version")
 
 
@@ -78,6 +78,7 @@ def _load():
     lib.inpc_ctx_stage_times.argtypes = [P, ct.POINTER(ct.c_float), ct.POINTER(i64), i32,
                                          ct.POINTER(i32), ct.c_int]
     lib.inpc_ctx_forget_events.argtypes = [P]
+    lib.inpc_sort_single64.argtypes = [P, P, P, P, P, i64, P, P, i64, ct.POINTER(i64), P]
     lib.inpc_ctx_set_allocator.argtypes = [P, ALLOC_FN, FREE_FN, P]
     lib.inpc_stage_name.argtypes = [i32]
     lib.inpc_stage_name.restype = ct.c_char_p
@@ -271,6 +272,21 @@ class Context:
         out["sorted_idx"] = out["sorted_idx"][:Ft.value]
         out["F_t"] = Ft.value
         return out
+
+    def sort_single64(self, cfg: RasterCfg, cam, xyz, opacity, stream=None):
+        """NEXT f4: the original INPC ordering (4 copies per point, one 64-bit
+        radix sort by pixel then depth).  Returns (pixel_ranges [H*W+1],
+        sorted_idx [F]) as int32 tensors (bit patterns of u32)."""
+        import torch
+        cam_arr, _ = _cams(cam)
+        N = xyz.shape[0]
+        dev = xyz.device
+        ranges = torch.empty(cfg.H * cfg.W + 1, dtype=torch.int32, device=dev)
+        idx = torch.empty(max(4 * N, 1), dtype=torch.int32, device=dev)
+        F = ct.c_int64()
+        _check(lib.inpc_sort_single64(self._h, ct.byref(cfg), cam_arr, _ptr(xyz), _ptr(opacity), N,
+                                      _ptr(ranges), _ptr(idx), idx.numel(), ct.byref(F), _stream(stream)))
+        return ranges, idx[:F.value]
 
     def set_profiling(self, on=True):
         _check(lib.inpc_ctx_set_profiling(self._h, 1 if on else 0))

@@ -13,6 +13,7 @@
 
 #include "inpc_raster.h"
 #include "kernels.cuh"
+#include "single_sort.cuh"
 
 using namespace inpc;
 
@@ -46,11 +47,12 @@ enum Stage : int {
   kStBlendBwd,
   kStBin,
   kStShGrad,
+  kStSingleSort,
   kNumStages
 };
 const char* kStageNames[kNumStages] = {"memset",    "project_count", "scan_tiles", "scatter",
                                        "sort_big",  "blend_fwd",     "blend_bwd",  "bin_fused",
-                                       "sh_grad"};
+                                       "sh_grad",   "single_sort"};
 
 struct ViewState {
   Buf ranges, sorted_idx, T_final, last, dbg_key, dbg_tiles, scalars, rec, feat_eval;
@@ -70,6 +72,7 @@ struct inpc_ctx {
   int big_grid = 0;
   // scratch (shared by views, stream ordered)
   Buf zeroed, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg, g_eval;
+  Buf f4_rec, f4_keys, f4_vals, f4_keys2, f4_vals2, f4_hist, f4_scan, f4_misc;  // NEXT f4 baseline
   int bin_grid[3] = {0, 0, 0};  // cooperative grid of k_bin_bilinear<2,4,8>
   bool no_fused_bin = false;     // env INPC_NO_FUSED_BIN=1: separate binning kernels
   uint64_t entry_cap = 0;
@@ -166,7 +169,8 @@ struct AllocScope {
 
 void release_all(inpc_ctx* c) {
   for (Buf* b : {&c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots,
-                 &c->agg, &c->g_eval, &c->tmp, &c->overflow})
+                 &c->agg, &c->g_eval, &c->tmp, &c->overflow, &c->f4_rec, &c->f4_keys, &c->f4_vals,
+                 &c->f4_keys2, &c->f4_vals2, &c->f4_hist, &c->f4_scan, &c->f4_misc})
     free_buf(*b);
   for (auto& v : c->views)
     for (Buf* b : {&v.ranges, &v.sorted_idx, &v.T_final, &v.last, &v.dbg_key, &v.dbg_tiles, &v.scalars,
@@ -839,6 +843,95 @@ int inpc_debug_export(inpc_ctx* c, int32_t view, uint32_t* depth_keys, uint32_t*
     int64_t n = Ft < sorted_cap ? Ft : sorted_cap;
     if (n > 0) CK(cudaMemcpyAsync(sorted_idx, vs.sorted_idx.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
   }
+  return INPC_OK;
+}
+
+int inpc_sort_single64(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camera* cam, const float* xyz,
+                       const float* opacity, int64_t N, uint32_t* pixel_ranges, uint32_t* sorted_idx,
+                       int64_t sorted_cap, int64_t* F_out, void* stream) {
+  if (!c) return INPC_INVALID_ARG;
+  int st = validate_cfg(cfg, cam, 1);
+  if (st) return st;
+  if (cfg->splat_mode != INPC_SPLAT_BILINEAR) return INPC_UNSUPPORTED;
+  if (N < 0 || 4 * N >= 0xFFFFFFFFll) return N < 0 ? INPC_INVALID_ARG : INPC_KEY_OVERFLOW;
+  DeviceGuard dg(c->device);
+  if (N > 0 && (!is_device_ptr(xyz) || !is_device_ptr(opacity))) return INPC_INVALID_ARG;
+  if (!is_device_ptr(pixel_ranges) || (sorted_idx && !is_device_ptr(sorted_idx))) return INPC_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  c->last_stream = s;
+  cudaGetLastError();
+  AllocScope alloc_scope(c);
+  DevCam dc;
+  DevCfg g;
+  make_dev(cfg, *cam, dc, g);
+  g.ty0 = 0;
+  g.ty1 = g.tiles_y;
+  g.flags &= ~(kFlagSH | kFlagEnv);
+  const int64_t P = (int64_t)cfg->H * cfg->W;
+  const int64_t n = 4 * N;
+  const int tiles = (int)((n + kRxTile - 1) / kRxTile);
+  const int64_t hist_n = (int64_t)256 * tiles;
+  const int scan_blocks = (int)((hist_n + kScanTile - 1) / kScanTile);
+  bool fresh = false;
+  if ((st = ensure(c->f4_rec, (size_t)(N > 0 ? N : 1) * sizeof(PointRec), s))) return st;
+  if ((st = ensure(c->f4_keys, (size_t)(n > 0 ? n : 1) * 8, s))) return st;
+  if ((st = ensure(c->f4_keys2, (size_t)(n > 0 ? n : 1) * 8, s))) return st;
+  if ((st = ensure(c->f4_vals, (size_t)(n > 0 ? n : 1) * 4, s))) return st;
+  if ((st = ensure(c->f4_vals2, (size_t)(n > 0 ? n : 1) * 4, s))) return st;
+  if ((st = ensure(c->f4_hist, (size_t)(hist_n > 0 ? hist_n : 1) * 4, s))) return st;
+  if ((st = ensure(c->f4_scan, (size_t)scan_blocks * 8 + sizeof(ScanCtl) + 16, s, &fresh))) return st;
+  if (fresh) CK(cudaMemsetAsync(c->f4_scan.p, 0, c->f4_scan.bytes, s));
+  if ((st = ensure(c->f4_misc, 64, s))) return st;
+  unsigned long long* nvalid = (unsigned long long*)c->f4_misc.p;
+  CK(cudaMemsetAsync(nvalid, 0, 8, s));
+  unsigned long long* state = (unsigned long long*)c->f4_scan.p;
+  ScanCtl* ctl = (ScanCtl*)(state + scan_blocks);
+  if (N > 0) {  // H1: the point records (not part of the timed sort)
+    const int nblk = (int)((N + (int64_t)kPointThreads * kPPT - 1) / ((int64_t)kPointThreads * kPPT));
+    k_project_count<0, false><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, nullptr, false, N,
+                                                              (PointRec*)c->f4_rec.p, nullptr, nullptr,
+                                                              nullptr, nullptr, nullptr);
+    CK(cudaGetLastError());
+  }
+  unsigned long long* ka = (unsigned long long*)c->f4_keys.p;
+  unsigned long long* kb = (unsigned long long*)c->f4_keys2.p;
+  uint32_t* va = (uint32_t*)c->f4_vals.p;
+  uint32_t* vb = (uint32_t*)c->f4_vals2.p;
+  {
+    StageTimer tm(c, s, kStSingleSort, 0);
+    if (N > 0) {
+      k_emit_pixel_frags<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(g, (const PointRec*)c->f4_rec.p, N, ka, va,
+                                                                      nvalid);
+      int pbits = 0;
+      while ((1ll << pbits) < P) ++pbits;
+      const int passes = (32 + pbits + 7) / 8;  // ceil((32 + 21) / 8) = 7 at 1080p
+      const int rblocks = (tiles + kRxWarps - 1) / kRxWarps;
+      for (int q = 0; q < passes; ++q) {
+        const int shift = 8 * q;
+        k_rx_hist<<<rblocks, kRxWarps * 32, 0, s>>>(ka, n, shift, tiles, (uint32_t*)c->f4_hist.p);
+        k_scan_u32<<<scan_blocks, kScanThreads, 0, s>>>(hist_n, (uint32_t*)c->f4_hist.p, state, ctl);
+        k_rx_scatter<<<rblocks, kRxWarps * 32, 0, s>>>(ka, va, n, shift, tiles, (const uint32_t*)c->f4_hist.p, kb,
+                                                        vb);
+        c->stage_launches[kStSingleSort] += 3;
+        unsigned long long* tk = ka;
+        ka = kb;
+        kb = tk;
+        uint32_t* tv = va;
+        va = vb;
+        vb = tv;
+      }
+      c->stage_launches[kStSingleSort] += 1;
+    }
+    k_pixel_ranges<<<(unsigned)((n + 1 + 255) / 256), 256, 0, s>>>(ka, n, P, pixel_ranges);
+    c->stage_launches[kStSingleSort] += 1;
+    CK(cudaGetLastError());
+  }
+  CK(cudaMemcpyAsync(c->host_scalars, nvalid, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t F = (int64_t)(*(unsigned long long*)c->host_scalars);
+  if (F_out) *F_out = F;
+  if (sorted_idx && F > 0)
+    CK(cudaMemcpyAsync(sorted_idx, va, (size_t)(F < sorted_cap ? F : sorted_cap) * 4, cudaMemcpyDeviceToDevice, s));
   return INPC_OK;
 }
 

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
                                      (f.yhi / kTile - f.ylo / kTile + 1))
                         : 0u;
     }
-    if (!ok) continue;
+    if (!ok || !tile_count) continue;  // tile_count null: records only (f4 baseline)
     int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
     int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
     if (MODE == 0) {

@@ -386,3 +386,18 @@ def test_screen_bands_assemble_bit_exact(inpc, ctx):
             asm[:, b0 * 8:min(b1 * 8, H)] = o["F"][:, b0 * 8:min(b1 * 8, H)]
         torch.cuda.synchronize()
         assert torch.equal(asm, full["F"])
+
+
+# ------------------------------------------------------------------ NEXT f4
+@pytest.mark.parametrize("which", ["cfg1", "cfg2"])
+def test_single64_sort_baseline(inpc, ctx, which):
+    """f4: the original single 64-bit sort gives exactly the
+    oracle's O7 per-pixel lists (and so the tiled path's per-pixel order)."""
+    c = synthgen.config1() if which == "cfg1" else synthgen.config2()
+    H, W = c["H"], c["W"]
+    cfg = inpc.make_cfg(H, W, 4)
+    r, idx = ctx.sort_single64(cfg, c["cams"][0], dev(c["xyz"]), dev(c["opacity"]))
+    torch.cuda.synchronize()
+    ro, io = oracle.pixel_lists(c["cams"][0], c["xyz"], H, W, method=1)
+    np.testing.assert_array_equal(r.cpu().numpy().view(np.uint32), ro)
+    np.testing.assert_array_equal(idx.cpu().numpy().view(np.uint32), io)
