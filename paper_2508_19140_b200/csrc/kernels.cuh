@@ -855,8 +855,6 @@ template <int CMAX>
 struct ChunkSmem {
   int xy[32];                   // bilinear block origin, x0 | y0 << 16
   float ac[32][4];              // bilinear alpha = min(o w, alpha_max) per block corner
-  float gw[32][4];              // bilinear dalpha/do per corner: w, or 0 where clamped
-  float rc[32][4];              // bilinear 1 / (1 - alpha) per corner (backward)
   float u[32], v[32], ca[32], cb[32], cc[32];  // Gaussian
   float o[32], z[32];
   float f[32][CMAX];
@@ -882,6 +880,8 @@ struct BwdSmem {
   static constexpr bool kSlots = MODE == 0;
   static constexpr int kStride = kSlots ? 9 : CMAX + 2;  // odd: no bank conflicts
   ChunkSmem<CMAX> ch;
+  float gw[32][4];   // bilinear dalpha/do per corner: w, or 0 where clamped
+  float rc[32][4];   // bilinear 1 / (1 - alpha) per corner
   float Gs[64][CMAX];
   float acc[32][kStride];
   int touched[32];
@@ -912,7 +912,8 @@ __device__ __forceinline__ EntryRegs load_entry(const DevCfg& g, const PointRec*
 template <int MODE, int CMAX, bool BWD>
 __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const DevCfg& g,
                                             const EntryRegs& r, const float* __restrict__ feat,
-                                            bool packed, int tx0, int ty0) {
+                                            bool packed, int tx0, int ty0, float* gw_out = nullptr,
+                                            float* rc_out = nullptr) {
   const float4 A = r.A, B = r.B;
   const uint32_t idx = r.idx;
   Foot f;
@@ -934,8 +935,8 @@ __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const
     }
     *reinterpret_cast<float4*>(&cs.ac[lane][0]) = make_float4(al[0], al[1], al[2], al[3]);
     if (BWD) {
-      *reinterpret_cast<float4*>(&cs.gw[lane][0]) = make_float4(gw[0], gw[1], gw[2], gw[3]);
-      *reinterpret_cast<float4*>(&cs.rc[lane][0]) =
+      *reinterpret_cast<float4*>(gw_out) = make_float4(gw[0], gw[1], gw[2], gw[3]);
+      *reinterpret_cast<float4*>(rc_out) =
           make_float4(__frcp_rn(__fsub_rn(1.0f, al[0])), __frcp_rn(__fsub_rn(1.0f, al[1])),
                       __frcp_rn(__fsub_rn(1.0f, al[2])), __frcp_rn(__fsub_rn(1.0f, al[3])));
     }
@@ -974,7 +975,7 @@ __device__ __forceinline__ bool entry_alpha(const ChunkSmem<CMAX>& cs, const Dev
     const int xy = cs.xy[e];
     corner = 2 * (py - (xy >> 16)) + (px - (int)(short)(xy & 0xFFFF));
     alpha = cs.ac[e][corner];
-    gw = cs.gw[e][corner];
+    gw = 0.0f;  // forward only: the backward reads its packed corner data
     return true;
   } else {
     corner = 0;
@@ -1237,17 +1238,26 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
   while (m) {
     const int e = 31 - __clz(m);
     m &= ~(1u << e);
-    float alpha, gw;
-    int corner;
-    if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, alpha, gw, corner)) continue;
+    float alpha, gw, one_m, rcp;
+    int corner = 0;
+    if (MODE == 0) {
+      const int xy = cs.xy[e];
+      corner = 2 * (py - (xy >> 16)) + (px - (int)(short)(xy & 0xFFFF));
+      alpha = cs.ac[e][corner];
+      gw = S.gw[e][corner];
+      rcp = S.rc[e][corner];
+      one_m = __fsub_rn(1.0f, alpha);
+    } else {
+      if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, alpha, gw, corner)) continue;
+      one_m = __fsub_rn(1.0f, alpha);
+      rcp = __frcp_rn(one_m);
+    }
     if ((g.flags & kFlagSkipZero) && alpha == 0.0f) continue;
-    const float one_m = __fsub_rn(1.0f, alpha);
-    // T_k from the staged reciprocal plus one Newton correction of the
-    // residual (as accurate as the IEEE division on 0 <= alpha < 1, without
-    // its special-case branch).  The recovery error grows with the list
-    // length; the plain 2-ulp fast division fails the 1e-3 gate on
-    // 40k-fragment pixels.
-    const float rcp = MODE == 0 ? cs.rc[e][corner] : __frcp_rn(one_m);
+    // T_k = T_{k+1} / (1 - alpha_k) from the staged reciprocal plus one
+    // Newton correction of the residual (as accurate as the IEEE division on
+    // 0 <= alpha < 1, without its special-case branch).  The recovery error
+    // grows with the list length; the plain 2-ulp fast division fails the
+    // 1e-3 gate on 40k-fragment pixels.
     const float q0 = s.T * rcp;
     const float Tk = fmaf(fmaf(-q0, one_m, s.T), rcp, q0);
     float gf = 0.0f;
@@ -1324,7 +1334,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CMAX <= 4 ? 7 : 1) k_blen
     if (e < tmax) {
       idx = __ldg(sorted_idx + begin + e);
       const EntryRegs r = load_entry<CMAX>(g, rec, feat, packed, idx);
-      stage_entry<MODE, CMAX, true>(cs, lane, g, r, feat, packed, tx0, ty0);
+      stage_entry<MODE, CMAX, true>(cs, lane, g, r, feat, packed, tx0, ty0, &S.gw[lane][0], &S.rc[lane][0]);
     }
     __syncwarp();
     bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane] & below_mask(a.last, base), px, pyA, a);
