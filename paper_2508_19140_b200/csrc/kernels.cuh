@@ -191,7 +191,7 @@ struct ViewScalars {
   uint32_t Ft;       // total tile entries
   uint32_t num_big;  // tiles with more than kWarpSortCap entries (reset by k_sort_big)
   uint32_t max_big;  // largest of them
-  uint32_t pad;
+  uint32_t pad;      // big-tile chunk dispenser (k_sort_big), zero between calls
 };
 
 // Scan bookkeeping, zero on entry and left zero on exit (the last CTA to
@@ -402,12 +402,13 @@ __device__ __forceinline__ void block_bitonic(unsigned long long* s, int np) {
     }
 }
 
-// Compare-exchange steps j = jmax .. 1 (j < 64) of bitonic level k on the
-// 64-element segment held by a warp in registers: element i = seg + 32 r +
-// lane in v[r]; the direction uses the global index i.
-__device__ __forceinline__ void seg_bitonic_low(unsigned long long (&v)[2], int seg, int k, int jmax,
-                                                int lane) {
-  for (int j = jmax; j > 0; j >>= 1) {
+// Compare-exchange steps j = JMAX .. 1 (JMAX <= 32) of bitonic level k on
+// the 64-element segment held by a warp in registers: element i = seg + 32 r
+// + lane in v[r]; the direction uses the global index i.  Fully unrolled.
+template <int JMAX>
+__device__ __forceinline__ void seg_bitonic_low(unsigned long long (&v)[2], int seg, int k, int lane) {
+#pragma unroll
+  for (int j = JMAX; j > 0; j >>= 1) {
     if (j == 32) {
       const bool up = ((seg + lane) & k) == 0;  // bit 5 clear for r = 0
       const unsigned long long a = v[0], b = v[1];
@@ -435,7 +436,12 @@ __device__ __forceinline__ void block_bitonic_fast(unsigned long long* s, int np
   // levels k <= 64 entirely in registers
   for (int seg = wid * 64; seg < np; seg += nw * 64) {
     unsigned long long v[2] = {s[seg + lane], s[seg + 32 + lane]};
-    for (int k = 2; k <= 64; k <<= 1) seg_bitonic_low(v, seg, k, k >> 1, lane);
+    seg_bitonic_low<1>(v, seg, 2, lane);
+    seg_bitonic_low<2>(v, seg, 4, lane);
+    seg_bitonic_low<4>(v, seg, 8, lane);
+    seg_bitonic_low<8>(v, seg, 16, lane);
+    seg_bitonic_low<16>(v, seg, 32, lane);
+    seg_bitonic_low<32>(v, seg, 64, lane);
     s[seg + lane] = v[0];
     s[seg + 32 + lane] = v[1];
   }
@@ -456,7 +462,7 @@ __device__ __forceinline__ void block_bitonic_fast(unsigned long long* s, int np
     }
     for (int seg = wid * 64; seg < np; seg += nw * 64) {
       unsigned long long v[2] = {s[seg + lane], s[seg + 32 + lane]};
-      seg_bitonic_low(v, seg, k, 32, lane);
+      seg_bitonic_low<32>(v, seg, k, lane);
       s[seg + lane] = v[0];
       s[seg + 32 + lane] = v[1];
     }
@@ -607,7 +613,10 @@ __device__ __forceinline__ void big_sort_body(
   }
   grid.sync();
   const uint32_t total_chunks = big_chunk[nb], total = big_elem[nb], maxn = sc->max_big;
-  for (uint32_t gch = blockIdx.x; gch < total_chunks; gch += gridDim.x) {
+  // chunks handed out dynamically (sizes vary by tile): carry[0] is this CTA's next chunk
+  if (threadIdx.x == 0) carry[0] = atomicAdd(&sc->pad, 1u);
+  __syncthreads();
+  for (uint32_t gch = carry[0]; gch < total_chunks;) {
     const uint32_t j = upper_bound_u32(big_chunk, nb, gch) - 1;
     const uint32_t t = big_tiles[j];
     const uint32_t c = gch - big_chunk[j];
@@ -624,7 +633,9 @@ __device__ __forceinline__ void big_sort_body(
     } else {
       for (int k = threadIdx.x; k < (int)n; k += blockDim.x) entries[begin + k] = s[k];
     }
+    if (threadIdx.x == 0) carry[0] = atomicAdd(&sc->pad, 1u);
     __syncthreads();
+    gch = carry[0];
   }
   if (total > 0) {  // tiles over one chunk: pairwise merges of the sorted runs
     grid.sync();
@@ -665,6 +676,7 @@ __device__ __forceinline__ void big_sort_body(
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     sc->num_big = 0u;
     sc->max_big = 0u;
+    sc->pad = 0u;
   }
 }
 
