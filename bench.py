@@ -48,18 +48,20 @@ def peaks():
 
 
 # ------------------------------------------------------------------ byte model
-def algorithmic_bytes(N, Nv, Ft, P, C, sh=False, env=False):
+def algorithmic_bytes(N, Nv, Ft, P, C, sh=False, env=False, Fbig=0):
     """Compulsory bytes per stage: each datum the method must
     move, counted once, whatever the implementation re-reads.  (Sums over
     views: N, Nv, Ft, P are totals.)  sh: features come as 9 SH coefficients
     per channel (read 36 C B per visible point, gradient written 36 C B);
-    env: a C-channel background value per pixel, read in fwd and bwd."""
+    env: a C-channel background value per pixel, read in fwd and bwd.
+    Fbig: entries of tiles longer than the blend's in-warp sort (256), which
+    the big-tile sort reads once (8 B key) and writes once (4 B index)."""
     fbytes = (36 if sh else 4) * C
     m = {
         "project_count": 12 * N + (fbytes * Nv if sh else 0),   # positions (+ SH coefficients)
         "scan_tiles": 0,
         "scatter": 8 * Ft,                             # one write of the (key, idx) record
-        "sort_big": 0,
+        "sort_big": 12 * Fbig,
         "blend_fwd": 8 * Ft + (4 + (0 if sh else 4 * C)) * Nv + 4 * P * (C + 2) + 8 * P,
         #            record read, opacity+features, F/A/D write, T_final+last write
         "blend_bwd": 4 * P * (C + 2) + 8 * P + 4 * Ft + (16 + 4 * C) * Nv + 4 * (C + 1) * Nv,
@@ -348,13 +350,15 @@ def run_ours(args, rank, world, local_rank):
     # workload statistics (untimed): visible points, tile entries, per view
     dbg = inpc.make_cfg(H, W, C, mode, flags=flags | inpc.FLAG_DEBUG, env_hw=env_hw)
     ctx.forward(dbg, cams, xyz, feat, op, bg=env_t)
-    Nv = Ft = 0
+    Nv = Ft = Fbig = 0
     for v in range(V):
         ex = ctx.debug_export(v, N=N, H=H, W=W)
         Nv += int((ex["tiles_touched"] > 0).sum().item())
         Ft += int(ex["F_t"])
+        cnt = ex["tile_ranges"][1:].long() - ex["tile_ranges"][:-1].long()
+        Fbig += int(cnt[cnt > 256].sum().item())
     model = algorithmic_bytes(N * V, Nv, Ft, P * V, C, sh="sh" in args.variant,
-                              env="env" in args.variant)
+                              env="env" in args.variant, Fbig=Fbig)
     if fwd_only:
         model = {k: v for k, v in model.items() if k not in ("blend_bwd", "sh_grad")}
     step_bytes = sum(model.values())
@@ -446,7 +450,9 @@ def run_ours(args, rank, world, local_rank):
             "bytes_per_launch": dom_bytes, "us_per_launch": dom_ms * 1e3}
     prof_traffic = os.path.join(ROOT, "profiles", "traffic_r01.json")
     if os.path.exists(prof_traffic):
-        tr = json.load(open(prof_traffic)).get(dom)
+        trj = json.load(open(prof_traffic))
+        key = f"cfg{args.config}" + ("" if args.variant == "base" else "-" + args.variant)
+        tr = trj.get(key, {}).get(dom)
         if tr:
             roof["traffic"] = tr
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
@@ -557,7 +563,7 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": {5: WORKLOAD5, 3: WORKLOAD3, 4: WORKLOAD4}.get(args.config, WORKLOAD),
                        "variant": args.variant, "N": N, "views_per_rank": V,
-                       "N_visible": Nv, "F_t": Ft, "H": H, "W": W,
+                       "N_visible": Nv, "F_t": Ft, "F_big": Fbig, "H": H, "W": W,
                        "C": C, "mode": mode, "alpha_max": 0.99, "t_min": 1e-4,
                        "parallelism": (f"64 views split over {world} ranks + gradient all-reduce"
                                        if args.config == 5 else

@@ -866,6 +866,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
 template <int CMAX>
 struct ChunkSmem {
   int xy[32];                   // bilinear block origin, x0 | y0 << 16
+  int cbase[32];                // bilinear corner base: corner = cb + 2 ly + lx at tile pixel (lx, ly)
   float ac[32][4];              // bilinear alpha = min(o w, alpha_max) per block corner
   float u[32], v[32], ca[32], cb[32], cc[32];  // Gaussian
   float o[32], z[32];
@@ -935,6 +936,7 @@ __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const
   cs.z[lane] = A.z;
   if (MODE == 0) {
     cs.xy[lane] = (f.x0 & 0xFFFF) | (f.y0 << 16);
+    cs.cbase[lane] = -(2 * (f.y0 - ty0) + (f.x0 - tx0));
     const float fa1 = __fsub_rn(1.0f, f.fa), fb1 = __fsub_rn(1.0f, f.fb);
     const float w[4] = {__fmul_rn(fa1, fb1), __fmul_rn(f.fa, fb1), __fmul_rn(fa1, f.fb),
                         __fmul_rn(f.fa, f.fb)};
@@ -972,8 +974,17 @@ __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const
   // footprint rectangle clipped to the tile, tile-local coordinates
   const int xl = max(f.xlo, tx0) - tx0, xh = min(f.xhi, tx0 + kTile - 1) - tx0;
   const int yl = max(f.ylo, ty0) - ty0, yh = min(f.yhi, ty0 + kTile - 1) - ty0;
-  for (int yy = yl; yy <= yh; ++yy)
-    for (int xx = xl; xx <= xh; ++xx) atomicOr(&cs.mask[yy * kTile + xx], 1u << lane);
+  if (MODE == 0) {  // the 2x2 block: four predicated marks, no loops
+    const int bx = f.x0 - tx0, by = f.y0 - ty0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int xx = bx + (k & 1), yy = by + (k >> 1);
+      if (xx >= xl && xx <= xh && yy >= yl && yy <= yh) atomicOr(&cs.mask[yy * kTile + xx], 1u << lane);
+    }
+  } else {
+    for (int yy = yl; yy <= yh; ++yy)
+      for (int xx = xl; xx <= xh; ++xx) atomicOr(&cs.mask[yy * kTile + xx], 1u << lane);
+  }
 }
 
 // Fragment of staged entry e at pixel (px, py): alpha (R4, R5), dalpha/do
@@ -981,11 +992,10 @@ __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const
 // every pixel of the rectangle is a fragment.  Gaussian: q <= 9 (R17).
 template <int MODE, int CMAX>
 __device__ __forceinline__ bool entry_alpha(const ChunkSmem<CMAX>& cs, const DevCfg& g, int e,
-                                            int px, int py, float& alpha, float& gw,
+                                            int px, int py, int pc, float& alpha, float& gw,
                                             int& corner) {
   if (MODE == 0) {
-    const int xy = cs.xy[e];
-    corner = 2 * (py - (xy >> 16)) + (px - (int)(short)(xy & 0xFFFF));
+    corner = cs.cbase[e] + pc;  // pc = 2 ly + lx of the pixel in its tile
     alpha = cs.ac[e][corner];
     gw = 0.0f;  // forward only: the backward reads its packed corner data
     return true;
@@ -1048,7 +1058,7 @@ struct PixFwd {
 // list order), Eq. 1 with alpha clamp (R5) and early termination (R6).
 template <int MODE, int CMAX, bool COUNT>
 __device__ __forceinline__ void blend_pixel(const ChunkSmem<CMAX>& cs, const DevCfg& g,
-                                            uint32_t m, int px, int py, uint32_t base,
+                                            uint32_t m, int px, int py, int pc, uint32_t base,
                                             PixFwd<CMAX>& s) {
   const bool count = COUNT;
   if (s.done && !count) return;
@@ -1057,7 +1067,7 @@ __device__ __forceinline__ void blend_pixel(const ChunkSmem<CMAX>& cs, const Dev
     m &= m - 1;
     float alpha, gw;
     int corner;
-    if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, alpha, gw, corner)) continue;
+    if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, pc, alpha, gw, corner)) continue;
     if (COUNT) s.nfrag++;
     if (s.done) continue;
     const float Tn = __fmul_rn(s.T, __fsub_rn(1.0f, alpha));
@@ -1132,6 +1142,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_fwd(
   const int tile = g.ty0 * g.tiles_x + tl;
   const int tx0 = (tile % g.tiles_x) * kTile, ty0 = (tile / g.tiles_x) * kTile;
   const int px = tx0 + (lane & 7), pyA = ty0 + (lane >> 3), pyB = pyA + 4;
+  const int pcA = 2 * (lane >> 3) + (lane & 7);  // 2 ly + lx of pixel A (B: + 8)
   const bool inA = px < g.W && pyA < g.H, inB = px < g.W && pyB < g.H;
   const uint32_t begin = ranges[tile], n = ranges[tile + 1] - begin;
   const bool small = n <= (uint32_t)kWarpSortCap;
@@ -1163,8 +1174,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_fwd(
       stage_entry<MODE, CMAX, false>(cs, lane, g, r, feat, packed, tx0, ty0);
     }
     __syncwarp();
-    blend_pixel<MODE, CMAX, COUNT>(cs, g, cs.mask[lane], px, pyA, base, a);
-    blend_pixel<MODE, CMAX, COUNT>(cs, g, cs.mask[lane + 32], px, pyB, base, b);
+    blend_pixel<MODE, CMAX, COUNT>(cs, g, cs.mask[lane], px, pyA, pcA, base, a);
+    blend_pixel<MODE, CMAX, COUNT>(cs, g, cs.mask[lane + 32], px, pyB, pcA + 8, base, b);
     __syncwarp();
     if (!count && __all_sync(0xffffffffu, a.done && b.done)) break;
   }
@@ -1244,7 +1255,7 @@ __device__ __forceinline__ void load_pixel_bwd(const DevCam& cam, const DevCfg& 
 // as the background).  alpha = 0 fragments are processed (R13).
 template <int MODE, int CMAX>
 __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& g, uint32_t m,
-                                          int px, int py, PixBwd<CMAX>& s) {
+                                          int px, int py, int pc, PixBwd<CMAX>& s) {
   using SM = BwdSmem<MODE, CMAX>;
   const ChunkSmem<CMAX>& cs = S.ch;
   while (m) {
@@ -1253,14 +1264,13 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
     float alpha, gw, one_m, rcp;
     int corner = 0;
     if (MODE == 0) {
-      const int xy = cs.xy[e];
-      corner = 2 * (py - (xy >> 16)) + (px - (int)(short)(xy & 0xFFFF));
+      corner = cs.cbase[e] + pc;
       alpha = cs.ac[e][corner];
       gw = S.gw[e][corner];
       rcp = S.rc[e][corner];
       one_m = __fsub_rn(1.0f, alpha);
     } else {
-      if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, alpha, gw, corner)) continue;
+      if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, pc, alpha, gw, corner)) continue;
       one_m = __fsub_rn(1.0f, alpha);
       rcp = __frcp_rn(one_m);
     }
@@ -1323,6 +1333,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CMAX <= 4 ? 7 : 1) k_blen
   const int tile = g.ty0 * g.tiles_x + tl;
   const int tx0 = (tile % g.tiles_x) * kTile, ty0 = (tile / g.tiles_x) * kTile;
   const int px = tx0 + (lane & 7), pyA = ty0 + (lane >> 3), pyB = pyA + 4;
+  const int pcA = 2 * (lane >> 3) + (lane & 7);  // 2 ly + lx of pixel A (B: + 8)
   const bool inA = px < g.W && pyA < g.H, inB = px < g.W && pyB < g.H;
   const uint32_t begin = ranges[tile];
   PixBwd<CMAX> a, b;
@@ -1349,8 +1360,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CMAX <= 4 ? 7 : 1) k_blen
       stage_entry<MODE, CMAX, true>(cs, lane, g, r, feat, packed, tx0, ty0, &S.gw[lane][0], &S.rc[lane][0]);
     }
     __syncwarp();
-    bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane] & below_mask(a.last, base), px, pyA, a);
-    bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane + 32] & below_mask(b.last, base), px, pyB, b);
+    bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane] & below_mask(a.last, base), px, pyA, pcA, a);
+    bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane + 32] & below_mask(b.last, base), px, pyB, pcA + 8, b);
     __syncwarp();
     if (e < tmax && S.touched[lane]) {
       float gsum[CMAX + 1];
