@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libinpc_raster.so")
 SOURCES = [os.path.join(CSRC, "inpc_raster.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "raster_math.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "raster_math.cuh", "single_sort.cuh")] + [
     os.path.join(ROOT, "include", "inpc_raster.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -35,7 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, *SOURCES, "-o", tmp]
+    extra = os.environ.get("INPC_NVCC_EXTRA", "").split()   # diagnostics only, e.g. -DINPC_PHASE_TIMES
+    cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC, *SOURCES, "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -633,7 +633,24 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       void* fn = fused_kp == 2 ? (void*)k_bin_bilinear<2, false>
                  : fused_kp == 4 ? (void*)k_bin_bilinear<4, false>
                                  : (void*)k_bin_bilinear<8, false>;
+#ifdef INPC_PHASE_TIMES
+      {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbolAsync(g_bin_ts, z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
+      }
+#endif
       CK(cudaLaunchCooperativeKernel(fn, fused_grid, kBinThreads, args, 0, s));
+#ifdef INPC_PHASE_TIMES
+      {
+        unsigned long long ts[8];
+        cudaMemcpyFromSymbolAsync(ts, g_bin_ts, sizeof(ts), 0, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "bin phases us: project %.1f scan %.1f scatter %.1f prefix %.1f chunks %.1f end %.1f\n",
+                (ts[1] - ts[0]) * 1e-3, (ts[2] - ts[1]) * 1e-3, (ts[3] - ts[2]) * 1e-3,
+                ts[4] ? (ts[4] - ts[3]) * 1e-3 : 0.0, ts[5] ? (ts[5] - ts[3]) * 1e-3 : 0.0,
+                ts[7] ? (ts[7] - ts[0]) * 1e-3 : 0.0);
+      }
+#endif
     }
     if (N > 0 && !fused_kp) {
       StageTimer tm(c, s, kStProject, 1);

@@ -560,6 +560,21 @@ __device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a,
 // search; keys are unique), (3) the point indices go to sorted_idx.  Grid-
 // synchronised between phases; returns at once if no tile is big.  Any
 // block size <= kBigThreads; s holds kBigChunk keys.
+#ifdef INPC_PHASE_TIMES  // diagnostics: %globaltimer at the phase boundaries of k_bin_bilinear
+__device__ unsigned long long g_bin_ts[8];
+#define BIN_TS(k)                                                                      \
+  do {                                                                                 \
+    if (threadIdx.x == 0) {                                                            \
+      unsigned long long t_;                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+      if (blockIdx.x == 0 && (k) < 4) g_bin_ts[k] = t_;                                \
+      if ((k) >= 4) atomicMax(&g_bin_ts[k], t_);                                       \
+    }                                                                                  \
+  } while (0)
+#else
+#define BIN_TS(k) do { } while (0)
+#endif
+
 template <int CHUNK>
 __device__ __forceinline__ void big_sort_body(
     cooperative_groups::grid_group& grid, unsigned long long* s, uint32_t* carry,
@@ -612,6 +627,7 @@ __device__ __forceinline__ void big_sort_body(
     __syncthreads();
   }
   grid.sync();
+  BIN_TS(4);
   const uint32_t total_chunks = big_chunk[nb], total = big_elem[nb], maxn = sc->max_big;
   // chunks handed out dynamically (sizes vary by tile): carry[0] is this CTA's next chunk
   if (threadIdx.x == 0) carry[0] = atomicAdd(&sc->pad, 1u);
@@ -637,6 +653,7 @@ __device__ __forceinline__ void big_sort_body(
     __syncthreads();
     gch = carry[0];
   }
+  BIN_TS(5);
   if (total > 0) {  // tiles over one chunk: pairwise merges of the sorted runs
     grid.sync();
     unsigned long long* src = entries;
@@ -724,6 +741,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
   __shared__ uint32_t wt[kBinThreads / 32];
   const int64_t nthr = (int64_t)gridDim.x * kBinThreads;
   const int64_t tid = (int64_t)blockIdx.x * kBinThreads + threadIdx.x;
+  BIN_TS(0);
   // ---- phase 1
   uint32_t key[KP], tb[KP], sl[KP][4], vm[KP];
 #pragma unroll
@@ -765,6 +783,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
     }
   }
   grid.sync();
+  BIN_TS(1);
   // ---- phase 2: CTA b scans tiles [b*per, (b+1)*per)
   const int per = (T + gridDim.x - 1) / gridDim.x;
   const int t0 = blockIdx.x * per, t1 = min(T, t0 + per);
@@ -823,6 +842,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
   }
   if (mx) atomicMax(&sc->max_big, mx);
   grid.sync();
+  BIN_TS(2);
   if (blockIdx.x == 0) {  // grand total = F_t
     uint32_t tot = 0;
     for (int b = threadIdx.x; b < (int)gridDim.x; b += kBinThreads) tot += agg[b];
@@ -851,9 +871,11 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
       }
   }
   grid.sync();
+  BIN_TS(3);
   // ---- phase 4: big tiles
   big_sort_body<kBigChunk>(grid, s, carry, ranges, big_tiles, big_elem, big_chunk, sc, entries, tmp,
                            sorted_idx);
+  BIN_TS(7);
 }
 
 // ---------------------------------------------------------------- H7 / H8 per-warp staging
