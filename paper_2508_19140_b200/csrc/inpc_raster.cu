@@ -393,8 +393,9 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   int per_sm = 0;
-  const int big_smem = kBigChunkLarge * 8;
+  const int big_smem = kBigChunkLarge * 8 + kRadixSmemU32 * 4;
   cudaFuncSetAttribute(k_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, big_smem);
+  cudaFuncSetAttribute(k_sort_big, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_big, kBigThreadsLarge, big_smem);
   c->big_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
   {
@@ -717,7 +718,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       uint32_t* si = (uint32_t*)vs.sorted_idx.p;
       void* args[] = {(void*)&r, (void*)&bt, (void*)&be, (void*)&bc, (void*)&scc, (void*)&en, (void*)&tp, (void*)&si};
       CK(cudaLaunchCooperativeKernel((void*)k_sort_big, c->big_grid, kBigThreadsLarge, args,
-                                     (size_t)kBigChunkLarge * 8, s));
+                                     (size_t)kBigChunkLarge * 8 + kRadixSmemU32 * 4, s));
     }
     {
       StageTimer tm(c, s, kStBlendFwd, 1);

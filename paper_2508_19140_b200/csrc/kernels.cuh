@@ -575,12 +575,19 @@ __device__ unsigned long long g_bin_ts[8];
 #define BIN_TS(k) do { } while (0)
 #endif
 
+constexpr int kRadixItems = 8;
+constexpr int kRadixMinN = 2048;  // smaller chunks: the bitonic network is cheaper than the passes
+constexpr int kRadixMaxRun = 64;
+constexpr int kRadixStride = 257;  // hist row stride (digit-major scan reads are conflict-free)
+constexpr int kRadixSmemU32 = 32 * kRadixStride + 32 + 4;
+__device__ __forceinline__ bool block_radix_depth(unsigned long long* s, int n, uint32_t* sm);
+
 template <int CHUNK>
 __device__ __forceinline__ void big_sort_body(
     cooperative_groups::grid_group& grid, unsigned long long* s, uint32_t* carry,
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles,
     uint32_t* big_elem, uint32_t* big_chunk, ViewScalars* sc, unsigned long long* entries,
-    unsigned long long* tmp, uint32_t* __restrict__ sorted_idx) {
+    unsigned long long* tmp, uint32_t* __restrict__ sorted_idx, uint32_t* radix_smem = nullptr) {
   const uint32_t nb = *(volatile uint32_t*)&sc->num_big;
   if (nb == 0) return;
   if (blockIdx.x == 0) {
@@ -630,10 +637,14 @@ __device__ __forceinline__ void big_sort_body(
   BIN_TS(4);
   const uint32_t total_chunks = big_chunk[nb], total = big_elem[nb], maxn = sc->max_big;
   // chunks handed out dynamically (sizes vary by tile): carry[0] is this CTA's next chunk
-  if (threadIdx.x == 0) carry[0] = atomicAdd(&sc->pad, 1u);
+  // (thread 0 draws the chunk and finds its tile: carry = {chunk, list slot})
+  if (threadIdx.x == 0) {
+    carry[0] = atomicAdd(&sc->pad, 1u);
+    carry[1] = carry[0] < total_chunks ? upper_bound_u32(big_chunk, nb, carry[0]) - 1 : 0u;
+  }
   __syncthreads();
   for (uint32_t gch = carry[0]; gch < total_chunks;) {
-    const uint32_t j = upper_bound_u32(big_chunk, nb, gch) - 1;
+    const uint32_t j = carry[1];
     const uint32_t t = big_tiles[j];
     const uint32_t c = gch - big_chunk[j];
     const uint32_t tn = ranges[t + 1] - ranges[t];
@@ -641,15 +652,29 @@ __device__ __forceinline__ void big_sort_body(
     const uint32_t n = min((uint32_t)CHUNK, ranges[t + 1] - begin);
     int np = 64;  // sort network of the next power of two, not the full chunk
     while (np < (int)n) np <<= 1;
-    for (int k = threadIdx.x; k < np; k += blockDim.x) s[k] = k < (int)n ? entries[begin + k] : ~0ull;
-    __syncthreads();
-    block_bitonic_fast(s, np);
+    bool sorted = false;
+    if (radix_smem && n > (uint32_t)kRadixMinN) {
+      for (int k = threadIdx.x; k < (int)n; k += blockDim.x) s[k] = entries[begin + k];
+      __syncthreads();
+      sorted = block_radix_depth(s, (int)n, radix_smem);
+      if (!sorted) {
+        for (int k = (int)n + threadIdx.x; k < np; k += blockDim.x) s[k] = ~0ull;
+        __syncthreads();
+      }
+    } else {
+      for (int k = threadIdx.x; k < np; k += blockDim.x) s[k] = k < (int)n ? entries[begin + k] : ~0ull;
+      __syncthreads();
+    }
+    if (!sorted) block_bitonic_fast(s, np);
     if (tn <= (uint32_t)CHUNK) {  // one chunk = the whole tile: final order
       for (int k = threadIdx.x; k < (int)n; k += blockDim.x) sorted_idx[begin + k] = (uint32_t)s[k];
     } else {
       for (int k = threadIdx.x; k < (int)n; k += blockDim.x) entries[begin + k] = s[k];
     }
-    if (threadIdx.x == 0) carry[0] = atomicAdd(&sc->pad, 1u);
+    if (threadIdx.x == 0) {
+      carry[0] = atomicAdd(&sc->pad, 1u);
+      carry[1] = carry[0] < total_chunks ? upper_bound_u32(big_chunk, nb, carry[0]) - 1 : 0u;
+    }
     __syncthreads();
     gch = carry[0];
   }
@@ -697,21 +722,164 @@ __device__ __forceinline__ void big_sort_body(
   }
 }
 
+// CTA radix sort of n <= 1024 * kRadixItems 64-bit keys (depth bits << 32 |
+// point index) in SMEM, for k_sort_big (1024 threads).  LSD passes of 8-bit
+// digits over the depth bits that vary in this chunk only (a tile's depths
+// share exponent and leading mantissa bits: 3 passes on cfg 4), each pass
+// stable: warp w owns elements [32 E w, 32 E (w+1)) in rounds of 32, lanes
+// with the same digit rank themselves with __match_any_sync, per-(digit,
+// warp) counts are scanned digit-major.  The keys of a pass sit in
+// registers, so the scatter goes back into s in place.  Stability keeps equal
+// depths in input order; runs of equal depth are then put in index order by
+// one thread each (insertion sort).  Returns false (s unchanged in content,
+// order undefined) when a run is longer than kRadixMaxRun: the caller then
+// sorts the chunk with the 64-bit bitonic network.
+
+__device__ __forceinline__ bool block_radix_depth(unsigned long long* s, int n, uint32_t* sm) {
+  uint32_t* hist = sm;                       // [32 warps][kRadixStride]
+  uint32_t* wsum = sm + 32 * kRadixStride;   // [32]
+  uint32_t* misc = wsum + 32;                // [0] OR, [1] AND, [2] long-run flag
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int E = (n + 1023) >> 10;
+  const int wbase = w * 32 * E;
+  unsigned long long kv[kRadixItems];
+  uint32_t o = 0u, a = 0xFFFFFFFFu;
+#pragma unroll
+  for (int r = 0; r < kRadixItems; ++r) {
+    const int i = wbase + r * 32 + lane;
+    kv[r] = 0ull;
+    if (r < E && i < n) {
+      kv[r] = s[i];
+      const uint32_t d = (uint32_t)(kv[r] >> 32);
+      o |= d;
+      a &= d;
+    }
+  }
+  if (threadIdx.x == 0) {
+    misc[0] = 0u;
+    misc[1] = 0xFFFFFFFFu;
+    misc[2] = 0u;
+  }
+  __syncthreads();
+  o = __reduce_or_sync(0xffffffffu, o);
+  a = __reduce_and_sync(0xffffffffu, a);
+  if (lane == 0) {
+    atomicOr(&misc[0], o);
+    atomicAnd(&misc[1], a);
+  }
+  __syncthreads();
+  const uint32_t vary = misc[0] ^ misc[1];
+  if (vary) {
+    const int lo = __ffs(vary) - 1, hi = 31 - __clz(vary);
+    for (int sh = lo; sh <= hi; sh += 8) {
+      uint32_t rank[kRadixItems];
+      for (int d = lane; d < 256; d += 32) hist[w * kRadixStride + d] = 0u;
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < kRadixItems; ++r) {
+        if (r >= E) break;
+        const int i = wbase + r * 32 + lane;
+        const bool valid = i < n;
+        const uint32_t d = valid ? (uint32_t)(kv[r] >> (32 + sh)) & 255u : 256u + lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        uint32_t cnt = 0;  // the leader advances the warp's counter of d; SMEM atomics keep rounds in order
+        if (valid && lane == leader) cnt = atomicAdd(&hist[w * kRadixStride + d], (uint32_t)__popc(peers));
+        cnt = __shfl_sync(0xffffffffu, cnt, leader);
+        rank[r] = cnt + __popc(peers & lt);
+      }
+      __syncthreads();
+      {  // exclusive scan of the counts in (digit, warp) order: thread t = 4 d + q owns warps 8q..8q+7
+        const int d = threadIdx.x >> 2, q = threadIdx.x & 3;
+        uint32_t c[8], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          c[k] = hist[(8 * q + k) * kRadixStride + d];
+          sum += c[k];
+        }
+        uint32_t x = sum;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+          if (lane >= off) x += y;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        if (w == 0) {
+          uint32_t v = wsum[lane];
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane >= off) v += y;
+          }
+          wsum[lane] = v;
+        }
+        __syncthreads();
+        uint32_t run = (w ? wsum[w - 1] : 0u) + x - sum;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          hist[(8 * q + k) * kRadixStride + d] = run;
+          run += c[k];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < kRadixItems; ++r) {
+        if (r >= E) break;
+        const int i = wbase + r * 32 + lane;
+        if (i < n) s[hist[w * kRadixStride + ((uint32_t)(kv[r] >> (32 + sh)) & 255u)] + rank[r]] = kv[r];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < kRadixItems; ++r) {
+        if (r >= E) break;
+        const int i = wbase + r * 32 + lane;
+        if (i < n) kv[r] = s[i];
+      }
+    }
+  }
+  // equal depths: index order within each run (runs are short; long ones fall back)
+  for (int p = threadIdx.x; p + 1 < n; p += blockDim.x) {
+    const uint32_t dp = (uint32_t)(s[p] >> 32);
+    if ((uint32_t)(s[p + 1] >> 32) != dp || (p > 0 && (uint32_t)(s[p - 1] >> 32) == dp)) continue;
+    int end = p + 2;
+    while (end < n && (uint32_t)(s[end] >> 32) == dp && end - p <= kRadixMaxRun) ++end;
+    if (end - p > kRadixMaxRun) {
+      misc[2] = 1u;
+      continue;
+    }
+    for (int k = p + 1; k < end; ++k) {
+      const unsigned long long v = s[k];
+      int j = k - 1;
+      while (j >= p && s[j] > v) {
+        s[j + 1] = s[j];
+        --j;
+      }
+      s[j + 1] = v;
+    }
+  }
+  __syncthreads();
+  return misc[2] == 0u;
+}
+
 // Stand-alone big-tile sort: 1024 threads, chunks of kBigChunkLarge keys in
-// 64 KB of dynamic SMEM, so tiles up to 8192 entries (cfg 4: 7750 tiles of
-// 2-7k entries) sort in one chunk without merge passes.
+// 64 KB of dynamic SMEM (+ the radix counters), so tiles up to 8192 entries
+// (cfg 4: 7750 tiles of 2-7k entries) sort in one chunk without merge passes;
+// chunks are sorted by block_radix_depth (bitonic fallback on long ties).
 constexpr int kBigChunkLarge = 8192;
 constexpr int kBigThreadsLarge = 1024;
-__global__ void __launch_bounds__(kBigThreadsLarge) k_sort_big(
+__global__ void __launch_bounds__(kBigThreadsLarge, 2) k_sort_big(
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles,
     uint32_t* big_elem, uint32_t* big_chunk, ViewScalars* sc,
     unsigned long long* entries, unsigned long long* tmp, uint32_t* __restrict__ sorted_idx) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t carry[2];
   unsigned long long* s = reinterpret_cast<unsigned long long*>(smem_raw);
+  uint32_t* rs = reinterpret_cast<uint32_t*>(s + kBigChunkLarge);
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   big_sort_body<kBigChunkLarge>(grid, s, carry, ranges, big_tiles, big_elem, big_chunk, sc, entries, tmp,
-                                sorted_idx);
+                                sorted_idx, rs);
 }
 
 // ---------------------------------------------------------------- H1..H6 fused (bilinear)
