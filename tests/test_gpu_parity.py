@@ -179,14 +179,22 @@ def test_all_culled(inpc, ctx):
 
 
 @pytest.mark.parametrize("n", [1500, 5000, 40000])
-def test_one_hot_tile_over_smem_cap(inpc, ctx, n):
+def test_one_hot_tile_over_smem_cap(inpc, ctx, n, ties="long"):
     """Degenerate skew: every point in one 8x8 tile -> the tile list exceeds
-    the in-SMEM sort cap and goes through k_sort_big's chunk sort + merges."""
+    the in-SMEM sort cap and goes through the big-tile chunk sort + merges.
+    ties: "long" = 10% of the points share one depth (a run over the radix
+    tie fix-up's limit), "short" = pairs and triples of equal depths, "none"."""
     rng = np.random.default_rng(n)
     W = H = 64
     cam = synthgen.camera(np.eye(3), np.zeros(3), 64.0, 64.0, 32, 32, 0.1)
     u = rng.uniform(17, 23, n); v = rng.uniform(9, 15, n); z = rng.uniform(1, 4, n)
-    z[: n // 10] = 2.0                        # exact depth ties
+    if ties == "long":
+        z[: n // 10] = 2.0                    # exact depth ties
+    elif ties == "short":
+        k = n // 6
+        z[k:2 * k] = z[:k]                    # pairs
+        z[2 * k:3 * k] = z[:k]                # and triples, scattered over the list
+        rng.shuffle(z)
     xyz = np.stack([(u - 32) / 64 * z, (v - 32) / 64 * z, z], 1).astype(np.float32)
     c = dict(xyz=xyz, feat=rng.uniform(-1, 1, (n, 4)).astype(np.float32),
              opacity=rng.uniform(0, 0.05, n).astype(np.float32), cams=[cam], H=H, W=W,
@@ -286,8 +294,12 @@ def test_unfused_binning_cfg2(inpc, ctx_unfused):
     run_full(inpc, ctx_unfused, synthgen.config2())
 
 
-def test_unfused_big_tile(inpc, ctx_unfused):
-    test_one_hot_tile_over_smem_cap(inpc, ctx_unfused, 5000)
+@pytest.mark.parametrize("n,ties", [(5000, "long"), (6000, "short"), (6000, "none"), (3000, "short"),
+                                    (20000, "short"), (2100, "none")])
+def test_unfused_big_tile(inpc, ctx_unfused, n, ties):
+    """k_sort_big: radix chunks (> 2048 entries) with short tie runs fixed up
+    in index order, the bitonic fallback for a long run, multi-chunk merges."""
+    test_one_hot_tile_over_smem_cap(inpc, ctx_unfused, n, ties)
 
 
 # ------------------------------------------------------------------ NEXT f1 / f2
