@@ -522,15 +522,104 @@ __device__ __forceinline__ void warp_sort_k(unsigned long long* keys,
   __syncwarp();
 }
 
+// 32-bit register bitonic (same network as reg_bitonic, half the shuffles
+// and compares of the 64-bit keys).
+template <int K>
+__device__ __forceinline__ void reg_bitonic32(uint32_t (&v)[K], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * K; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int jr = j >> 5;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          if ((r & jr) == 0) {
+            const int r2 = r | jr;
+            const bool up = ((r * 32) & k) == 0;
+            const uint32_t a = v[r], b = v[r2];
+            const bool sw = (a > b) == up;
+            v[r] = sw ? b : a;
+            v[r2] = sw ? a : b;
+          }
+        }
+      } else {
+        const bool lower = (lane & j) == 0;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], j);
+          const bool up = ((r * 32 + lane) & k) == 0;
+          v[r] = (lower == up) ? min(o, v[r]) : max(o, v[r]);
+        }
+      }
+    }
+  }
+}
+
+// Tile-list sort through 32-bit keys: (depth bits - tile minimum) shifted to
+// 24 bits, then the 8-bit list slot.  That order equals the (depth, index)
+// order unless two entries share a truncated depth; the result is checked
+// for order on the full 64-bit keys and, if any adjacent pair is out of
+// order, re-sorted with the 64-bit network (exactly the same result).
+template <int K>
+__device__ __forceinline__ void warp_sort_k32(unsigned long long* keys,
+                                              const unsigned long long* __restrict__ src, int n,
+                                              int lane) {
+  unsigned long long f[K];
+  uint32_t dmin = 0xFFFFFFFFu, dmax = 0u;
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int i = r * 32 + lane;
+    f[r] = i < n ? src[i] : ~0ull;
+    if (i < n) {
+      const uint32_t d = (uint32_t)(f[r] >> 32);
+      dmin = min(dmin, d);
+      dmax = max(dmax, d);
+      keys[i] = f[r];
+    }
+  }
+  dmin = __reduce_min_sync(0xffffffffu, dmin);
+  dmax = __reduce_max_sync(0xffffffffu, dmax);
+  const uint32_t range = dmax - dmin;
+  const int shift = max(0, (32 - __clz(range)) - 24);
+  uint32_t v[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int i = r * 32 + lane;
+    v[r] = i < n ? ((((uint32_t)(f[r] >> 32) - dmin) >> shift) << 8) | (uint32_t)i : 0xFFFFFFFFu;
+  }
+  reg_bitonic32<K>(v, lane);
+  __syncwarp();
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int i = r * 32 + lane;
+    f[r] = i < n ? keys[v[r] & 255u] : ~0ull;
+  }
+#pragma unroll
+  for (int r = 0; r < K; ++r) {  // element i + 1 is lane + 1 of row r, or lane 0 of row r + 1
+    unsigned long long nx = __shfl_down_sync(0xffffffffu, f[r], 1);
+    const unsigned long long nr = __shfl_sync(0xffffffffu, f[r + 1 < K ? r + 1 : r], 0);
+    if (lane == 31) nx = nr;
+    const int i = r * 32 + lane;
+    if (i + 1 < n && f[r] > nx) bad = true;
+  }
+  if (__any_sync(0xffffffffu, bad)) reg_bitonic<K>(f, lane);
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < K; ++r) keys[r * 32 + lane] = f[r];
+  __syncwarp();
+}
+
 // Warp-level sort of n <= kWarpSortCap unique 64-bit (depth key, index)
 // keys read from src into keys[0..n) (SMEM), all in registers.
 __device__ __forceinline__ void warp_sort(unsigned long long* keys,
                                           const unsigned long long* __restrict__ src, int n,
                                           int lane) {
-  if (n <= 32) warp_sort_k<1>(keys, src, n, lane);
-  else if (n <= 64) warp_sort_k<2>(keys, src, n, lane);
-  else if (n <= 128) warp_sort_k<4>(keys, src, n, lane);
-  else warp_sort_k<8>(keys, src, n, lane);
+  if (n <= 32) warp_sort_k32<1>(keys, src, n, lane);
+  else if (n <= 64) warp_sort_k32<2>(keys, src, n, lane);
+  else if (n <= 128) warp_sort_k32<4>(keys, src, n, lane);
+  else warp_sort_k32<8>(keys, src, n, lane);
 }
 
 __device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
