@@ -1623,18 +1623,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CMAX <= 4 ? 7 : 1) k_blen
   for (int o = 16; o > 0; o >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
   if (tmax == 0) return;
   ChunkSmem<CMAX>& cs = S.ch;
-  for (int chunk = (int)((tmax - 1) >> 5); chunk >= 0; --chunk) {
+  const int chunk0 = (int)((tmax - 1) >> 5);
+  // the list index of the next chunk is loaded one chunk ahead (one register)
+  uint32_t idx_next = chunk0 * 32 + lane < tmax ? __ldg(sorted_idx + begin + chunk0 * 32 + lane) : 0u;
+  for (int chunk = chunk0; chunk >= 0; --chunk) {
     const uint32_t base = (uint32_t)chunk * 32;
     const uint32_t e = base + lane;
+    const uint32_t idx = idx_next;
+    if (chunk > 0) idx_next = __ldg(sorted_idx + begin + base - 32 + lane);
     cs.mask[lane] = 0u;
     cs.mask[lane + 32] = 0u;
 #pragma unroll
     for (int c = 0; c < SM::kStride; ++c) S.acc[lane][c] = 0.0f;
     S.touched[lane] = 0;
     __syncwarp();
-    uint32_t idx = 0;
     if (e < tmax) {
-      idx = __ldg(sorted_idx + begin + e);
       const EntryRegs r = load_entry<CMAX>(g, rec, feat, packed, idx);
       stage_entry<MODE, CMAX, true>(cs, lane, g, r, feat, packed, tx0, ty0, &S.gw[lane][0], &S.rc[lane][0]);
     }
