@@ -405,13 +405,13 @@ __device__ __forceinline__ void block_bitonic(unsigned long long* s, int np) {
 // Compare-exchange steps j = JMAX .. 1 (JMAX <= 32) of bitonic level k on
 // the 64-element segment held by a warp in registers: element i = seg + 32 r
 // + lane in v[r]; the direction uses the global index i.  Fully unrolled.
-template <int JMAX>
-__device__ __forceinline__ void seg_bitonic_low(unsigned long long (&v)[2], int seg, int k, int lane) {
+template <int JMAX, typename KT>
+__device__ __forceinline__ void seg_bitonic_low(KT (&v)[2], int seg, int k, int lane) {
 #pragma unroll
   for (int j = JMAX; j > 0; j >>= 1) {
     if (j == 32) {
       const bool up = ((seg + lane) & k) == 0;  // bit 5 clear for r = 0
-      const unsigned long long a = v[0], b = v[1];
+      const KT a = v[0], b = v[1];
       const bool sw = (a > b) == up;
       v[0] = sw ? b : a;
       v[1] = sw ? a : b;
@@ -419,7 +419,7 @@ __device__ __forceinline__ void seg_bitonic_low(unsigned long long (&v)[2], int 
       const bool lower = (lane & j) == 0;
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], j);
+        const KT o = __shfl_xor_sync(0xffffffffu, v[r], j);
         const bool up = ((seg + r * 32 + lane) & k) == 0;
         v[r] = (lower == up) ? (o < v[r] ? o : v[r]) : (o > v[r] ? o : v[r]);
       }
@@ -431,11 +431,12 @@ __device__ __forceinline__ void seg_bitonic_low(unsigned long long (&v)[2], int 
 // SMEM with most steps in registers: every step with partner distance < 64
 // runs on 64-key warp segments with shuffles, only the steps with distance
 // >= 64 go through SMEM with block barriers (10 of 55 barriers at np = 1024).
-__device__ __forceinline__ void block_bitonic_fast(unsigned long long* s, int np) {
+template <typename KT>
+__device__ __forceinline__ void block_bitonic_fast(KT* s, int np) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   // levels k <= 64 entirely in registers
   for (int seg = wid * 64; seg < np; seg += nw * 64) {
-    unsigned long long v[2] = {s[seg + lane], s[seg + 32 + lane]};
+    KT v[2] = {s[seg + lane], s[seg + 32 + lane]};
     seg_bitonic_low<1>(v, seg, 2, lane);
     seg_bitonic_low<2>(v, seg, 4, lane);
     seg_bitonic_low<4>(v, seg, 8, lane);
@@ -451,7 +452,7 @@ __device__ __forceinline__ void block_bitonic_fast(unsigned long long* s, int np
       for (int t = threadIdx.x; t < (np >> 1); t += blockDim.x) {
         const int i = 2 * t - (t & (j - 1));
         const int ixj = i + j;
-        const unsigned long long a = s[i], b = s[ixj];
+        const KT a = s[i], b = s[ixj];
         const bool up = (i & k) == 0;
         if ((a > b) == up) {
           s[i] = b;
@@ -461,7 +462,7 @@ __device__ __forceinline__ void block_bitonic_fast(unsigned long long* s, int np
       __syncthreads();
     }
     for (int seg = wid * 64; seg < np; seg += nw * 64) {
-      unsigned long long v[2] = {s[seg + lane], s[seg + 32 + lane]};
+      KT v[2] = {s[seg + lane], s[seg + 32 + lane]};
       seg_bitonic_low<32>(v, seg, k, lane);
       s[seg + lane] = v[0];
       s[seg + 32 + lane] = v[1];
@@ -670,6 +671,7 @@ constexpr int kRadixMaxRun = 64;
 constexpr int kRadixStride = 257;  // hist row stride (digit-major scan reads are conflict-free)
 constexpr int kRadixSmemU32 = 32 * kRadixStride + 32 + 4;
 __device__ __forceinline__ bool block_radix_depth(unsigned long long* s, int n, uint32_t* sm);
+__device__ __forceinline__ bool block_sort32_depth(unsigned long long* s, int n, int np, uint32_t* sm);
 
 template <int CHUNK>
 __device__ __forceinline__ void big_sort_body(
@@ -746,6 +748,14 @@ __device__ __forceinline__ void big_sort_body(
       for (int k = threadIdx.x; k < (int)n; k += blockDim.x) s[k] = entries[begin + k];
       __syncthreads();
       sorted = block_radix_depth(s, (int)n, radix_smem);
+      if (!sorted) {
+        for (int k = (int)n + threadIdx.x; k < np; k += blockDim.x) s[k] = ~0ull;
+        __syncthreads();
+      }
+    } else if (radix_smem && np <= 2 * (int)blockDim.x) {
+      for (int k = threadIdx.x; k < (int)n; k += blockDim.x) s[k] = entries[begin + k];
+      __syncthreads();
+      sorted = block_sort32_depth(s, (int)n, np, radix_smem);
       if (!sorted) {
         for (int k = (int)n + threadIdx.x; k < np; k += blockDim.x) s[k] = ~0ull;
         __syncthreads();
@@ -950,6 +960,72 @@ __device__ __forceinline__ bool block_radix_depth(unsigned long long* s, int n, 
   }
   __syncthreads();
   return misc[2] == 0u;
+}
+
+// Chunk sort through 32-bit keys for k_sort_big's small chunks (np <= 2
+// blockDim): (depth bits - chunk minimum) shifted into 32 - log2(np) bits,
+// then the slot.  Equal truncated depths may leave neighbours out of (depth,
+// index) order: up to four odd-even transposition passes on the full keys
+// repair that; returns false if the chunk is still unsorted (the caller then
+// runs the 64-bit network).
+__device__ __forceinline__ bool block_sort32_depth(unsigned long long* s, int n, int np, uint32_t* sm) {
+  uint32_t* u = sm;
+  uint32_t* misc = sm + 32 * kRadixStride + 32;
+  const int lane = threadIdx.x & 31;
+  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const uint32_t d = (uint32_t)(s[k] >> 32);
+    lo = min(lo, d);
+    hi = max(hi, d);
+  }
+  if (threadIdx.x == 0) {
+    misc[0] = 0xFFFFFFFFu;
+    misc[1] = 0u;
+  }
+  __syncthreads();
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if (lane == 0) {
+    atomicMin(&misc[0], lo);
+    atomicMax(&misc[1], hi);
+  }
+  __syncthreads();
+  const uint32_t dmin = misc[0], range = misc[1] - dmin;
+  const int sb = __ffs(np) - 1;
+  const int shift = max(0, (32 - __clz(range)) - (32 - sb));
+  for (int k = threadIdx.x; k < np; k += blockDim.x)
+    u[k] = k < n ? ((((uint32_t)(s[k] >> 32) - dmin) >> shift) << sb) | (uint32_t)k : 0xFFFFFFFFu;
+  __syncthreads();
+  block_bitonic_fast<uint32_t>(u, np);
+  unsigned long long f[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int k = threadIdx.x + r * blockDim.x;
+    f[r] = k < n ? s[u[k] & (uint32_t)(np - 1)] : 0ull;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int k = threadIdx.x + r * blockDim.x;
+    if (k < n) s[k] = f[r];
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 4; ++pass) {
+    int sw = 0;
+    for (int ph = 0; ph < 2; ++ph) {
+      for (int k = 2 * threadIdx.x + ph; k + 1 < n; k += 2 * blockDim.x) {
+        const unsigned long long a = s[k], b = s[k + 1];
+        if (a > b) {
+          s[k] = b;
+          s[k + 1] = a;
+          sw = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!__syncthreads_or(sw)) return true;
+  }
+  return false;
 }
 
 // Stand-alone big-tile sort: 1024 threads, chunks of kBigChunkLarge keys in

@@ -295,10 +295,12 @@ def test_unfused_binning_cfg2(inpc, ctx_unfused):
 
 
 @pytest.mark.parametrize("n,ties", [(5000, "long"), (6000, "short"), (6000, "none"), (3000, "short"),
-                                    (20000, "short"), (2100, "none")])
+                                    (20000, "short"), (2100, "none"), (1500, "short"), (1500, "long"),
+                                    (300, "none"), (2048, "short")])
 def test_unfused_big_tile(inpc, ctx_unfused, n, ties):
     """k_sort_big: radix chunks (> 2048 entries) with short tie runs fixed up
-    in index order, the bitonic fallback for a long run, multi-chunk merges."""
+    in index order, 32-bit-key bitonic chunks (<= 2048) with odd-even
+    repair, the 64-bit fallbacks for long runs, multi-chunk merges."""
     test_one_hot_tile_over_smem_cap(inpc, ctx_unfused, n, ties)
 
 
