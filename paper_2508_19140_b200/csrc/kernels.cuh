@@ -667,11 +667,13 @@ __device__ unsigned long long g_bin_ts[8];
 
 constexpr int kRadixItems = 8;
 constexpr int kRadixMinN = 2048;  // smaller chunks: the bitonic network is cheaper than the passes
+constexpr bool kUseRadix = true;  // chunks > kRadixMinN: radix (cfg 4: 1.15 ms vs 1.48 ms with 32-bit bitonic chunks)
 constexpr int kRadixMaxRun = 64;
 constexpr int kRadixStride = 257;  // hist row stride (digit-major scan reads are conflict-free)
 constexpr int kRadixSmemU32 = 32 * kRadixStride + 32 + 4;
 __device__ __forceinline__ bool block_radix_depth(unsigned long long* s, int n, uint32_t* sm);
-__device__ __forceinline__ bool block_sort32_depth(unsigned long long* s, int n, int np, uint32_t* sm);
+__device__ __forceinline__ bool block_sort32_depth(const unsigned long long* s, int n, int np, uint32_t* u,
+                                                   uint32_t* misc);
 
 template <int CHUNK>
 __device__ __forceinline__ void big_sort_body(
@@ -743,32 +745,33 @@ __device__ __forceinline__ void big_sort_body(
     const uint32_t n = min((uint32_t)CHUNK, ranges[t + 1] - begin);
     int np = 64;  // sort network of the next power of two, not the full chunk
     while (np < (int)n) np <<= 1;
-    bool sorted = false;
-    if (radix_smem && n > (uint32_t)kRadixMinN) {
+    bool sorted = false, perm = false;
+    uint32_t* u = radix_smem;                                  // 32-bit keys / permutation
+    uint32_t* misc = radix_smem ? radix_smem + 32 * kRadixStride + 32 : nullptr;
+    if (radix_smem && kUseRadix && n > (uint32_t)kRadixMinN) {
       for (int k = threadIdx.x; k < (int)n; k += blockDim.x) s[k] = entries[begin + k];
       __syncthreads();
       sorted = block_radix_depth(s, (int)n, radix_smem);
-      if (!sorted) {
-        for (int k = (int)n + threadIdx.x; k < np; k += blockDim.x) s[k] = ~0ull;
-        __syncthreads();
-      }
-    } else if (radix_smem && np <= 2 * (int)blockDim.x) {
+    } else if (radix_smem) {
       for (int k = threadIdx.x; k < (int)n; k += blockDim.x) s[k] = entries[begin + k];
       __syncthreads();
-      sorted = block_sort32_depth(s, (int)n, np, radix_smem);
-      if (!sorted) {
-        for (int k = (int)n + threadIdx.x; k < np; k += blockDim.x) s[k] = ~0ull;
-        __syncthreads();
-      }
-    } else {
-      for (int k = threadIdx.x; k < np; k += blockDim.x) s[k] = k < (int)n ? entries[begin + k] : ~0ull;
-      __syncthreads();
+      sorted = perm = block_sort32_depth(s, (int)n, np, u, misc);
     }
-    if (!sorted) block_bitonic_fast(s, np);
+    if (!sorted) {
+      if (radix_smem) {
+        for (int k = (int)n + threadIdx.x; k < np; k += blockDim.x) s[k] = ~0ull;
+      } else {
+        for (int k = threadIdx.x; k < np; k += blockDim.x) s[k] = k < (int)n ? entries[begin + k] : ~0ull;
+      }
+      __syncthreads();
+      block_bitonic_fast(s, np);
+    }
+    const uint32_t pm = (uint32_t)np - 1u;
     if (tn <= (uint32_t)CHUNK) {  // one chunk = the whole tile: final order
-      for (int k = threadIdx.x; k < (int)n; k += blockDim.x) sorted_idx[begin + k] = (uint32_t)s[k];
+      for (int k = threadIdx.x; k < (int)n; k += blockDim.x)
+        sorted_idx[begin + k] = (uint32_t)s[perm ? (u[k] & pm) : k];
     } else {
-      for (int k = threadIdx.x; k < (int)n; k += blockDim.x) entries[begin + k] = s[k];
+      for (int k = threadIdx.x; k < (int)n; k += blockDim.x) entries[begin + k] = s[perm ? (u[k] & pm) : k];
     }
     if (threadIdx.x == 0) {
       carry[0] = atomicAdd(&sc->pad, 1u);
@@ -962,15 +965,15 @@ __device__ __forceinline__ bool block_radix_depth(unsigned long long* s, int n, 
   return misc[2] == 0u;
 }
 
-// Chunk sort through 32-bit keys for k_sort_big's small chunks (np <= 2
-// blockDim): (depth bits - chunk minimum) shifted into 32 - log2(np) bits,
-// then the slot.  Equal truncated depths may leave neighbours out of (depth,
-// index) order: up to four odd-even transposition passes on the full keys
-// repair that; returns false if the chunk is still unsorted (the caller then
-// runs the 64-bit network).
-__device__ __forceinline__ bool block_sort32_depth(unsigned long long* s, int n, int np, uint32_t* sm) {
-  uint32_t* u = sm;
-  uint32_t* misc = sm + 32 * kRadixStride + 32;
+// Chunk sort through 32-bit keys for k_sort_big: u[k] = (depth bits - chunk
+// minimum) shifted into 32 - log2(np) bits, then the slot k.  The sorted u
+// is a permutation of s (s itself is not moved).  Equal truncated depths may
+// leave neighbours out of (depth, index) order: up to four odd-even
+// transposition passes over u, comparing the full keys s[slot], repair that;
+// returns false if the chunk is still unsorted (the caller then runs the
+// 64-bit network on s).
+__device__ __forceinline__ bool block_sort32_depth(const unsigned long long* s, int n, int np, uint32_t* u,
+                                                   uint32_t* misc) {
   const int lane = threadIdx.x & 31;
   uint32_t lo = 0xFFFFFFFFu, hi = 0u;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
@@ -992,32 +995,20 @@ __device__ __forceinline__ bool block_sort32_depth(unsigned long long* s, int n,
   __syncthreads();
   const uint32_t dmin = misc[0], range = misc[1] - dmin;
   const int sb = __ffs(np) - 1;
+  const uint32_t mask = (uint32_t)np - 1u;
   const int shift = max(0, (32 - __clz(range)) - (32 - sb));
   for (int k = threadIdx.x; k < np; k += blockDim.x)
     u[k] = k < n ? ((((uint32_t)(s[k] >> 32) - dmin) >> shift) << sb) | (uint32_t)k : 0xFFFFFFFFu;
   __syncthreads();
   block_bitonic_fast<uint32_t>(u, np);
-  unsigned long long f[2];
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int k = threadIdx.x + r * blockDim.x;
-    f[r] = k < n ? s[u[k] & (uint32_t)(np - 1)] : 0ull;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int k = threadIdx.x + r * blockDim.x;
-    if (k < n) s[k] = f[r];
-  }
-  __syncthreads();
   for (int pass = 0; pass < 4; ++pass) {
     int sw = 0;
     for (int ph = 0; ph < 2; ++ph) {
       for (int k = 2 * threadIdx.x + ph; k + 1 < n; k += 2 * blockDim.x) {
-        const unsigned long long a = s[k], b = s[k + 1];
-        if (a > b) {
-          s[k] = b;
-          s[k + 1] = a;
+        const uint32_t a = u[k], b = u[k + 1];
+        if ((a >> sb) == (b >> sb) && s[a & mask] > s[b & mask]) {
+          u[k] = b;
+          u[k + 1] = a;
           sw = 1;
         }
       }
