@@ -833,8 +833,12 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     }
     if (sh) {
       StageTimer tm(c, s, kStShGrad, 1);
-      k_sh_grad<<<(unsigned)((N + kShPts - 1) / kShPts), 256, 0, s>>>(dc, g, xyz, N, (const float*)c->g_eval.p,
-                                                            g_point_feat + (size_t)v * feat_view_stride);
+      float* gsh = g_point_feat + (size_t)v * feat_view_stride;
+      const unsigned nb = (unsigned)((N + kShPts - 1) / kShPts);
+      if (cfg->C == 4 && ((uintptr_t)gsh & 15u) == 0)
+        k_sh_grad<4><<<nb, 256, 0, s>>>(dc, g, xyz, N, (const float*)c->g_eval.p, gsh);
+      else
+        k_sh_grad<0><<<nb, 256, 0, s>>>(dc, g, xyz, N, (const float*)c->g_eval.p, gsh);
       CK(cudaGetLastError());
     }
   }

@@ -79,10 +79,13 @@ __device__ __forceinline__ void sh_point_features(const DevCam& cam, const DevCf
 }
 
 // NEXT f1 backward: dL/dcoeff[c][k] += dL/df_c Y_k(d)  (g_sh [N, C, 9]).
-// A block handles 32 points: their basis values and dL/df are staged in SMEM
-// and the 32*C*9 contiguous coefficient gradients are read-modify-written
-// with consecutive threads on consecutive floats (coalesced).
-constexpr int kShPts = 32;
+// A block handles kShPts points: their basis values and dL/df are staged in
+// SMEM and the kShPts*C*9 contiguous coefficient gradients are
+// read-modify-written with consecutive threads on consecutive floats
+// (C = 4: float4, 9 per point; divisions by constants).  Points whose dL/df
+// is zero (not visible) are not touched.
+constexpr int kShPts = 64;
+template <int CT>
 __global__ void __launch_bounds__(256) k_sh_grad(DevCam cam, DevCfg g, const float* __restrict__ xyz,
                                                  int64_t N, const float* __restrict__ g_f,
                                                  float* __restrict__ g_sh) {
@@ -90,18 +93,40 @@ __global__ void __launch_bounds__(256) k_sh_grad(DevCam cam, DevCfg g, const flo
   __shared__ float sG[kShPts * 64];
   const int64_t p0 = (int64_t)blockIdx.x * kShPts;
   const int np = (int)min((int64_t)kShPts, N - p0);
+  const int C = CT ? CT : g.C;
   if (threadIdx.x < np) {
     const int64_t i = p0 + threadIdx.x;
     sh_dir_basis(cam, __ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2), sB[threadIdx.x]);
   }
-  for (int j = threadIdx.x; j < np * g.C; j += blockDim.x) sG[j] = __ldg(g_f + p0 * g.C + j);
+  for (int j = threadIdx.x; j < np * C; j += blockDim.x) sG[j] = __ldg(g_f + p0 * C + j);
   __syncthreads();
-  const int per_pt = g.C * 9;
-  float* out = g_sh + p0 * per_pt;
-  for (int j = threadIdx.x; j < np * per_pt; j += blockDim.x) {
-    const int p = j / per_pt, r = j - p * per_pt, c = r / 9, k = r - c * 9;
-    const float gf = sG[p * g.C + c];
-    if (gf != 0.0f) out[j] += gf * sB[p][k];
+  if (CT == 4) {
+    float4* out4 = reinterpret_cast<float4*>(g_sh + p0 * 36);  // 144 B per point: 16-B aligned
+    for (int j4 = threadIdx.x; j4 < np * 9; j4 += blockDim.x) {
+      const int p = j4 / 9, r0 = 4 * (j4 - p * 9);
+      float gf[4], bk[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = r0 + q, c = r / 9, k = r - c * 9;
+        gf[q] = sG[p * 4 + c];
+        bk[q] = sB[p][k];
+      }
+      if (gf[0] == 0.0f && gf[1] == 0.0f && gf[2] == 0.0f && gf[3] == 0.0f) continue;
+      float4 v = out4[j4];
+      v.x += gf[0] * bk[0];
+      v.y += gf[1] * bk[1];
+      v.z += gf[2] * bk[2];
+      v.w += gf[3] * bk[3];
+      out4[j4] = v;
+    }
+  } else {
+    const int per_pt = C * 9;
+    float* out = g_sh + p0 * per_pt;
+    for (int j = threadIdx.x; j < np * per_pt; j += blockDim.x) {
+      const int p = j / per_pt, r = j - p * per_pt, c = r / 9, k = r - c * 9;
+      const float gf = sG[p * C + c];
+      if (gf != 0.0f) out[j] += gf * sB[p][k];
+    }
   }
 }
 
