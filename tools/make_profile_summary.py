@@ -15,7 +15,7 @@ import sys
 tag, launches = sys.argv[1], sys.argv[2]
 reports = [a.split("=", 1) for a in sys.argv[3:]]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-out_dir = os.path.join(ROOT, "profiles")
+out_dir = os.environ.get("PROFILE_OUT", os.path.join(ROOT, "profiles"))
 os.makedirs(out_dir, exist_ok=True)
 STAGE = {"k_project_count": "project_count", "k_scan_tiles": "scan_tiles", "k_scatter": "scatter",
          "k_scatter_slots": "scatter", "k_sort_big": "sort_big", "k_blend_fwd": "blend_fwd",

@@ -13,3 +13,14 @@ tools/prof_one.sh 5 "k_blend_bwd" final_cfg5 2
 tools/prof_one.sh 2 "k_blend_bwd" final_env 2 "--variant env"
 tools/prof_one.sh 2 "k_blend_bwd" final_sh 2 "--variant sh"
 ls -la gpurun_out/*.ncu-rep | tail -8
+# summaries on the box (the reports together exceed what gpurun brings back)
+PROFILE_OUT=gpurun_out/prof_out python tools/make_profile_summary.py r01 gpurun_out/launches_final.csv \
+    cfg2=gpurun_out/prof_final_cfg2.ncu-rep cfg3=gpurun_out/prof_final_cfg3.ncu-rep \
+    cfg4=gpurun_out/prof_final_cfg4.ncu-rep cfg5=gpurun_out/prof_final_cfg5.ncu-rep \
+    cfg2-env=gpurun_out/prof_final_env.ncu-rep cfg2-sh=gpurun_out/prof_final_sh.ncu-rep > /dev/null
+for k in cfg2:k_blend_bwd cfg2:k_blend_fwd cfg2:k_bin cfg3:k_blend_fwd cfg4:k_sort_big cfg5:k_blend_bwd; do
+  python tools/src_lines.py gpurun_out/prof_final_${k%%:*}.ncu-rep ${k##*:} 40 > gpurun_out/prof_out/src_${k%%:*}_${k##*:}.txt 2>&1
+  python tools/stall_regions.py gpurun_out/prof_final_${k%%:*}.ncu-rep ${k##*:} 4000 > gpurun_out/prof_out/stall_${k%%:*}_${k##*:}.txt 2>&1
+done
+mkdir -p /tmp/ncu_reps && mv gpurun_out/prof_final_cfg[345].ncu-rep gpurun_out/prof_final_env.ncu-rep gpurun_out/prof_final_sh.ncu-rep /tmp/ncu_reps/
+ls gpurun_out/prof_out
