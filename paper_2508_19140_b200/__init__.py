@@ -64,9 +64,14 @@ class RasterCfg(ct.Structure):
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with "
-                          "`python -m paper_2508_19140_b200.build` (nvcc, sm_100a); "
-                          "there is no CPU fallback")
+        # compile the sm_100a library in-tree (nvcc); without it there is no path at all
+        from . import build as _build
+        try:
+            _build.build()
+        except Exception as e:
+            raise ImportError(f"{LIB_PATH} is missing and could not be built ({e}); build it with "
+                              "`python -m paper_2508_19140_b200.build` (nvcc, sm_100a); "
+                              "there is no CPU fallback") from e
     lib = ct.CDLL(LIB_PATH)
     P, i32, i64 = ct.c_void_p, ct.c_int32, ct.c_int64
     lib.inpc_ctx_create.argtypes = [ct.POINTER(P), ct.c_int]
