@@ -291,17 +291,36 @@ void set_smem(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+template <int MODE, int CMAX, bool COUNT, int WPB>
+void launch_blend_fwd_w(int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
+                        const PointRec* rec, const float* feat, bool packed, const float* bg,
+                        const uint32_t* ranges, const unsigned long long* entries,
+                        uint32_t* sorted_idx, const BlendOut& o) {
+  const size_t smem = WPB * sizeof(FwdSmem<CMAX>);
+  static bool once = (set_smem(k_blend_fwd<MODE, CMAX, COUNT, WPB>, smem), true);
+  (void)once;
+  const int grid = (band_tiles + WPB - 1) / WPB;
+  k_blend_fwd<MODE, CMAX, COUNT, WPB><<<grid, WPB * 32, smem, s>>>(
+      dc, g, band_tiles, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
+}
+
+int env_wpb(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : kWarpsPerBlock;
+}
+
 template <int MODE, int CMAX, bool COUNT>
 void launch_blend_fwd_t(int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
                         const PointRec* rec, const float* feat, bool packed, const float* bg,
                         const uint32_t* ranges, const unsigned long long* entries,
                         uint32_t* sorted_idx, const BlendOut& o) {
-  const size_t smem = kWarpsPerBlock * sizeof(FwdSmem<CMAX>);
-  static bool once = (set_smem(k_blend_fwd<MODE, CMAX, COUNT>, smem), true);
-  (void)once;
-  const int grid = (band_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  k_blend_fwd<MODE, CMAX, COUNT><<<grid, kWarpsPerBlock * 32, smem, s>>>(
-      dc, g, band_tiles, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
+#ifdef INPC_FAST_BUILD
+  static const int w = env_wpb("INPC_WPB_FWD");
+  if (w == 1) return launch_blend_fwd_w<MODE, CMAX, COUNT, 1>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
+  if (w == 2) return launch_blend_fwd_w<MODE, CMAX, COUNT, 2>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
+  if (w == 8) return launch_blend_fwd_w<MODE, CMAX, COUNT, 8>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
+#endif
+  launch_blend_fwd_w<MODE, CMAX, COUNT, kWarpsPerBlock>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
 }
 
 template <int MODE, int CMAX>
@@ -318,16 +337,28 @@ void launch_blend_fwd(int band_tiles, cudaStream_t s, const DevCam& dc, const De
                                           sorted_idx, o);
 }
 
+template <int MODE, int CMAX, int WPB>
+void launch_blend_bwd_w(int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
+                        const PointRec* rec, const float* feat, bool packed, const float* bg,
+                        const uint32_t* ranges, const uint32_t* sorted_idx, const BwdIn& in) {
+  const size_t smem = WPB * sizeof(BwdSmem<MODE, CMAX>);
+  static bool once = (set_smem(k_blend_bwd<MODE, CMAX, WPB>, smem), true);
+  (void)once;
+  const int grid = (band_tiles + WPB - 1) / WPB;
+  k_blend_bwd<MODE, CMAX, WPB><<<grid, WPB * 32, smem, s>>>(dc, g, band_tiles, rec, feat, packed,
+                                                            bg, ranges, sorted_idx, in);
+}
+
 template <int MODE, int CMAX>
 void launch_blend_bwd(int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
                       const PointRec* rec, const float* feat, bool packed, const float* bg,
                       const uint32_t* ranges, const uint32_t* sorted_idx, const BwdIn& in) {
-  const size_t smem = kWarpsPerBlock * sizeof(BwdSmem<MODE, CMAX>);
-  static bool once = (set_smem(k_blend_bwd<MODE, CMAX>, smem), true);
-  (void)once;
-  const int grid = (band_tiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  k_blend_bwd<MODE, CMAX><<<grid, kWarpsPerBlock * 32, smem, s>>>(dc, g, band_tiles, rec, feat, packed,
-                                                                  bg, ranges, sorted_idx, in);
+#ifdef INPC_FAST_BUILD
+  static const int w = env_wpb("INPC_WPB_BWD");
+  if (w == 1) return launch_blend_bwd_w<MODE, CMAX, 1>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, sorted_idx, in);
+  if (w == 2) return launch_blend_bwd_w<MODE, CMAX, 2>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, sorted_idx, in);
+#endif
+  launch_blend_bwd_w<MODE, CMAX, kWarpsPerBlock>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, sorted_idx, in);
 }
 
 template <int MODE>
@@ -337,10 +368,14 @@ void dispatch_blend_fwd(int cmax, int band_tiles, cudaStream_t s, const DevCam& 
                         uint32_t* sorted_idx, const BlendOut& o) {
   switch (cmax) {
     case 4: launch_blend_fwd<MODE, 4>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+#ifndef INPC_FAST_BUILD  // diagnostics build: C <= 4 kernels only
     case 8: launch_blend_fwd<MODE, 8>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
     case 16: launch_blend_fwd<MODE, 16>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
     case 32: launch_blend_fwd<MODE, 32>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
     default: launch_blend_fwd<MODE, 64>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+#else
+    default: launch_blend_fwd<MODE, 4>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+#endif
   }
 }
 
@@ -350,10 +385,14 @@ void dispatch_blend_bwd(int cmax, int band_tiles, cudaStream_t s, const DevCam& 
                         const uint32_t* ranges, const uint32_t* sorted_idx, const BwdIn& in) {
   switch (cmax) {
     case 4: launch_blend_bwd<MODE, 4>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+#ifndef INPC_FAST_BUILD  // diagnostics build: C <= 4 kernels only
     case 8: launch_blend_bwd<MODE, 8>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
     case 16: launch_blend_bwd<MODE, 16>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
     case 32: launch_blend_bwd<MODE, 32>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
     default: launch_blend_bwd<MODE, 64>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+#else
+    default: launch_blend_bwd<MODE, 4>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, sorted_idx, in); break;
+#endif
   }
 }
 
@@ -400,9 +439,12 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
   c->big_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
   {
     int o2 = 0, o4 = 0, o8 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_bin_bilinear<2, false>, kBinThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k_bin_bilinear<4, false>, kBinThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o8, k_bin_bilinear<8, false>, kBinThreads, 0);
+    cudaFuncSetAttribute(k_bin_bilinear<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bin_smem_bytes<2>());
+    cudaFuncSetAttribute(k_bin_bilinear<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bin_smem_bytes<4>());
+    cudaFuncSetAttribute(k_bin_bilinear<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bin_smem_bytes<8>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_bin_bilinear<2, false>, kBinThreads, bin_smem_bytes<2>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k_bin_bilinear<4, false>, kBinThreads, bin_smem_bytes<4>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o8, k_bin_bilinear<8, false>, kBinThreads, bin_smem_bytes<8>());
     c->bin_grid[0] = c->num_sms * o2;
     c->bin_grid[1] = c->num_sms * o4;
     c->bin_grid[2] = c->num_sms * o8;
@@ -596,7 +638,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     // (measured on cfg 2 at 1080p: fused 58.5 us vs 67 us for the separate
     // kernels eagerly, and 201.5 vs 203.7 us per fwd+bwd step in a CUDA graph)
     int fused_kp = 0, fused_grid = 0;
-    if (!gauss && !sh && N > 0 && !c->no_fused_bin) {
+    if (!gauss && !sh && N > 0 && !c->no_fused_bin && T < (1 << 28)) {  // tile base + corner mask in 32 bits
       const int kps[3] = {2, 4, 8};
       for (int q = 0; q < 3; ++q)
         if (c->bin_grid[q] > 0 && N <= (int64_t)kps[q] * c->bin_grid[q] * kBinThreads) {
@@ -640,7 +682,8 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
         cudaMemcpyToSymbolAsync(g_bin_ts, z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
       }
 #endif
-      CK(cudaLaunchCooperativeKernel(fn, fused_grid, kBinThreads, args, 0, s));
+      const size_t bsm = fused_kp == 2 ? bin_smem_bytes<2>() : fused_kp == 4 ? bin_smem_bytes<4>() : bin_smem_bytes<8>();
+      CK(cudaLaunchCooperativeKernel(fn, fused_grid, kBinThreads, args, bsm, s));
 #ifdef INPC_PHASE_TIMES
       {
         unsigned long long ts[8];

@@ -1075,6 +1075,12 @@ __global__ void __launch_bounds__(kBigThreadsLarge, 2) k_sort_big(
 //   phase 4  H4/H6: tiles over the warp-sort cap (big_sort_body)
 constexpr int kBinThreads = 512;
 
+template <int KP>
+constexpr size_t bin_smem_bytes() {
+  return (size_t)KP * 4 * kBinThreads * 4 > (size_t)kBigChunk * 8 ? (size_t)KP * 4 * kBinThreads * 4
+                                                                   : (size_t)kBigChunk * 8;
+}
+
 template <int KP, bool SH>
 __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
     DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ opacity,
@@ -1085,52 +1091,92 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
     float* __restrict__ feat_out) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  __shared__ unsigned long long s[kBigChunk];
+  // dynamic SMEM (bin_smem_bytes<KP>()): the per-point tile slots of phases
+  // 1-3 ([k][corner][thread], conflict-free), then phase 4's sort chunk
+  extern __shared__ __align__(16) unsigned char bin_smem[];
+  unsigned long long* s = reinterpret_cast<unsigned long long*>(bin_smem);
+  uint32_t* s_sl = reinterpret_cast<uint32_t*>(bin_smem);
   __shared__ uint32_t carry[2];
   __shared__ uint32_t wt[kBinThreads / 32];
   const int64_t nthr = (int64_t)gridDim.x * kBinThreads;
   const int64_t tid = (int64_t)blockIdx.x * kBinThreads + threadIdx.x;
   BIN_TS(0);
   // ---- phase 1
-  uint32_t key[KP], tb[KP], sl[KP][4], vm[KP];
+  // per point in registers: depth key and tile base | corner mask << 28
+  // (T < 2^28); the slots wait in SMEM.  Software pipeline (issue is in
+  // order): the inputs of point k + 1 are loaded while point k is projected,
+  // and the slots returned by point k's atomics are stored to SMEM two points
+  // later, so that no instruction waits on an atomic's round trip.
+  constexpr int kDefer = 2;
+  uint32_t key[KP], tb[KP];
+  uint32_t psl[kDefer][4];
+  float nX = 0.f, nY = 0.f, nZ = 0.f, nO = 0.f;
+  float4 nF = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto load_in = [&](int64_t i) {
+    if (i < N) {
+      nX = __ldg(xyz + 3 * i);
+      nY = __ldg(xyz + 3 * i + 1);
+      nZ = __ldg(xyz + 3 * i + 2);
+      nO = __ldg(opacity + i);
+      if (!SH && pack) nF = __ldg(reinterpret_cast<const float4*>(feat) + i);
+    }
+  };
+  auto store_slots = [&](int k) {
+    const uint32_t vm = tb[k] >> 28;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if ((vm >> c) & 1u) s_sl[(k * 4 + c) * kBinThreads + threadIdx.x] = psl[k % kDefer][c];
+  };
+  load_in(tid);
 #pragma unroll
   for (int k = 0; k < KP; ++k) {
     const int64_t i = tid + k * nthr;
     key[k] = 0u;
-    vm[k] = 0u;
-    if (i >= N) continue;
-    Proj p;
-    Foot f;
-    const float X = __ldg(xyz + 3 * i), Y = __ldg(xyz + 3 * i + 1), Z = __ldg(xyz + 3 * i + 2);
-    const bool vis = project_point(cam, X, Y, Z, p);
-    const bool ok = vis && foot_bilinear(g, p.u, p.v, f);
-    PointRec pr;
-    pr.a = make_float4(p.u, p.v, ok ? p.zc : 0.0f, __ldg(opacity + i));
-    pr.b = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (SH) {
-      if (ok) sh_point_features(cam, g, feat, i, X, Y, Z, pack, pr.b, feat_out);
-    } else if (pack) {
-      pr.b = __ldg(reinterpret_cast<const float4*>(feat) + i);
-    }
-    rec[i] = pr;
-    if (dbg_key) {
-      dbg_key[i] = vis ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
-      dbg_tiles[i] = ok ? (uint32_t)((f.xhi / kTile - f.xlo / kTile + 1) * (f.yhi / kTile - f.ylo / kTile + 1)) : 0u;
-    }
-    if (!ok) continue;
-    const int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
-    const int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
-    key[k] = __float_as_uint(p.zc);
-    tb[k] = (uint32_t)(ty_lo * g.tiles_x + tx_lo);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int tx = tx_lo + (c & 1), ty = ty_lo + (c >> 1);
-      if (tx <= tx_hi && ty <= ty_hi) {
-        sl[k][c] = atomicAdd(counts + (size_t)ty * g.tiles_x + tx, 1u);
-        vm[k] |= 1u << c;
+    tb[k] = 0u;
+    const float X = nX, Y = nY, Z = nZ, O = nO;
+    const float4 Fv = nF;
+    if (k + 1 < KP) load_in(i + nthr);
+    if (i < N) {
+      Proj p;
+      Foot f;
+      const bool vis = project_point(cam, X, Y, Z, p);
+      const bool ok = vis && foot_bilinear(g, p.u, p.v, f);
+      PointRec pr;
+      pr.a = make_float4(p.u, p.v, ok ? p.zc : 0.0f, O);
+      pr.b = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (SH) {
+        if (ok) sh_point_features(cam, g, feat, i, X, Y, Z, pack, pr.b, feat_out);
+      } else if (pack) {
+        pr.b = Fv;
       }
+      rec[i] = pr;
+      if (dbg_key) {
+        dbg_key[i] = vis ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
+        dbg_tiles[i] = ok ? (uint32_t)((f.xhi / kTile - f.xlo / kTile + 1) * (f.yhi / kTile - f.ylo / kTile + 1)) : 0u;
+      }
+      if (k >= kDefer) store_slots(k - kDefer);
+      if (ok) {
+        const int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
+        const int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
+        key[k] = __float_as_uint(p.zc);
+        uint32_t vm = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int tx = tx_lo + (c & 1), ty = ty_lo + (c >> 1);
+          if (tx <= tx_hi && ty <= ty_hi) {
+            psl[k % kDefer][c] = atomicAdd(counts + (size_t)ty * g.tiles_x + tx, 1u);
+            vm |= 1u << c;
+          }
+        }
+        tb[k] = (uint32_t)(ty_lo * g.tiles_x + tx_lo) | (vm << 28);
+      }
+    } else if (k >= kDefer) {
+      store_slots(k - kDefer);
     }
   }
+#pragma unroll
+  for (int k = KP - kDefer; k < KP; ++k)
+    if (k >= 0) store_slots(k);
   grid.sync();
   BIN_TS(1);
   // ---- phase 2: CTA b scans tiles [b*per, (b+1)*per)
@@ -1212,11 +1258,12 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
     if (!key[k]) continue;
     const int64_t i = tid + k * nthr;
     const unsigned long long kv = ((unsigned long long)key[k] << 32) | (uint32_t)i;
+    const uint32_t t0 = tb[k] & 0x0FFFFFFFu;
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      if (vm[k] & (1u << c)) {
-        const uint32_t t = tb[k] + (uint32_t)(c & 1) + (uint32_t)(c >> 1) * g.tiles_x;
-        entries[ranges[t] + sl[k][c]] = kv;
+      if ((tb[k] >> (28 + c)) & 1u) {
+        const uint32_t t = t0 + (uint32_t)(c & 1) + (uint32_t)(c >> 1) * g.tiles_x;
+        entries[ranges[t] + s_sl[(k * 4 + c) * kBinThreads + threadIdx.x]] = kv;
       }
   }
   grid.sync();
@@ -1236,10 +1283,16 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
 //   Gaussian: u, v and the conic; the pixel lane evaluates q and w (R17)
 template <int CMAX>
 struct ChunkSmem {
-  int xy[32];                   // bilinear block origin, x0 | y0 << 16
-  int cbase[32];                // bilinear corner base: corner = cb + 2 ly + lx at tile pixel (lx, ly)
-  float ac[32][4];              // bilinear alpha = min(o w, alpha_max) per block corner
-  float u[32], v[32], ca[32], cb[32], cc[32];  // Gaussian
+  union {
+    struct {
+      int xy[32];               // bilinear block origin, x0 | y0 << 16
+      int cbase[32];            // bilinear corner base: corner = cb + 2 ly + lx at tile pixel (lx, ly)
+      float ac[32][4];          // bilinear alpha = min(o w, alpha_max) per block corner
+    };
+    struct {
+      float u[32], v[32], ca[32], cb[32], cc[32];  // Gaussian
+    };
+  };
   float o[32], z[32];
   float f[32][CMAX];
   uint32_t mask[64];
@@ -1265,11 +1318,19 @@ struct BwdSmem {
   static constexpr int kStride = kSlots ? 9 : CMAX + 2;  // odd: no bank conflicts
   ChunkSmem<CMAX> ch;
   float gw[32][4];   // bilinear dalpha/do per corner: w, or 0 where clamped
-  float rc[32][4];   // bilinear 1 / (1 - alpha) per corner
+  float rc[32][4];   // bilinear 1 / (1 - alpha) per corner (approximate: the recovery adds a Newton step)
   float Gs[64][CMAX];
   float acc[32][kStride];
   int touched[32];
 };
+
+// 1/x to ~1 ulp (MUFU.RCP; x in [0.01, 1] here): the backward's T recovery
+// corrects it with one Newton step of the residual
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 // The global loads of one tile-list entry, issued a chunk ahead of their
 // use (software pipelining: the warp works on chunk k while chunk k+1's
@@ -1322,8 +1383,8 @@ __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const
     if (BWD) {
       *reinterpret_cast<float4*>(gw_out) = make_float4(gw[0], gw[1], gw[2], gw[3]);
       *reinterpret_cast<float4*>(rc_out) =
-          make_float4(__frcp_rn(__fsub_rn(1.0f, al[0])), __frcp_rn(__fsub_rn(1.0f, al[1])),
-                      __frcp_rn(__fsub_rn(1.0f, al[2])), __frcp_rn(__fsub_rn(1.0f, al[3])));
+          make_float4(rcp_approx(__fsub_rn(1.0f, al[0])), rcp_approx(__fsub_rn(1.0f, al[1])),
+                      rcp_approx(__fsub_rn(1.0f, al[2])), rcp_approx(__fsub_rn(1.0f, al[3])));
     }
   } else {
     cs.u[lane] = A.x;
@@ -1499,8 +1560,8 @@ __device__ __forceinline__ void write_pixel(const DevCam& cam, const DevCfg& g, 
 
 // ---------------------------------------------------------------- H4/H6 (small tiles) + H7
 // One warp per 8x8 tile; lane l owns pixels (l & 7, l >> 3) and (l & 7, 4 + (l >> 3)).
-template <int MODE, int CMAX, bool COUNT>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_fwd(
+template <int MODE, int CMAX, bool COUNT, int WPB = kWarpsPerBlock>
+__global__ void __launch_bounds__(WPB * 32) k_blend_fwd(
     DevCam cam, DevCfg g, int band_tiles, const PointRec* __restrict__ rec,
     const float* __restrict__ feat, bool packed, const float* __restrict__ bg,
     const uint32_t* __restrict__ ranges, const unsigned long long* __restrict__ entries,
@@ -1508,7 +1569,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_blend_fwd(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   FwdSmem<CMAX>& S = reinterpret_cast<FwdSmem<CMAX>*>(smem_raw)[warp];
-  const int tl = blockIdx.x * kWarpsPerBlock + warp;
+  const int tl = blockIdx.x * WPB + warp;
   if (tl >= band_tiles) return;  // warp-uniform; no block barriers below
   const int tile = g.ty0 * g.tiles_x + tl;
   const int tx0 = (tile % g.tiles_x) * kTile, ty0 = (tile / g.tiles_x) * kTile;
@@ -1632,18 +1693,20 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
   while (m) {
     const int e = 31 - __clz(m);
     m &= ~(1u << e);
-    float alpha, gw, one_m, rcp;
+    float alpha, gw, one_m, rcp, z;
     int corner = 0;
     if (MODE == 0) {
       corner = cs.cbase[e] + pc;
       alpha = cs.ac[e][corner];
       gw = S.gw[e][corner];
       rcp = S.rc[e][corner];
+      z = cs.z[e];
       one_m = __fsub_rn(1.0f, alpha);
     } else {
       if (!entry_alpha<MODE, CMAX>(cs, g, e, px, py, pc, alpha, gw, corner)) continue;
       one_m = __fsub_rn(1.0f, alpha);
       rcp = __frcp_rn(one_m);
+      z = cs.z[e];
     }
     if ((g.flags & kFlagSkipZero) && alpha == 0.0f) continue;
     // T_k = T_{k+1} / (1 - alpha_k) from the staged reciprocal plus one
@@ -1661,20 +1724,20 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
 #pragma unroll
       for (int c = 0; c < CMAX; ++c) gf += s.G[c] * cs.f[e][c];
     }
-    const float z = cs.z[e];
     const float dA = Tk * ((gf - s.S) + s.GD * (z - s.SD) + s.GA * s.P);
     const float ta = Tk * alpha;
     const float go = gw * dA;  // dalpha/do = w, or 0 where the clamp is active
     if (SM::kSlots) {
       S.acc[e][2 * corner] = ta;  // odd row stride: scalar stores
       S.acc[e][2 * corner + 1] = go;
+      S.touched[e] = 1;
     } else {
 #pragma unroll
       for (int c = 0; c < CMAX; ++c)
         if (c < g.C) atomicAdd(&S.acc[e][c], ta * s.G[c]);
       atomicAdd(&S.acc[e][CMAX], go);
+      S.touched[e] = 1;
     }
-    S.touched[e] = 1;
     s.S = alpha * gf + one_m * s.S;
     s.SD = alpha * z + one_m * s.SD;
     s.P *= one_m;
@@ -1690,8 +1753,8 @@ __device__ __forceinline__ uint32_t below_mask(uint32_t last, uint32_t base) {
 }
 
 // 7 CTAs of 4 warps per SM (<= 73 registers): measured 82 vs 93 us at 6 CTAs on cfg 2
-template <int MODE, int CMAX>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, CMAX <= 4 ? 7 : 1) k_blend_bwd(
+template <int MODE, int CMAX, int WPB = kWarpsPerBlock>
+__global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? 28 / WPB : 1) k_blend_bwd(
     DevCam cam, DevCfg g, int band_tiles, const PointRec* __restrict__ rec,
     const float* __restrict__ feat, bool packed, const float* __restrict__ bg,
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ sorted_idx, BwdIn in) {
@@ -1699,7 +1762,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, CMAX <= 4 ? 7 : 1) k_blen
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   using SM = BwdSmem<MODE, CMAX>;
   SM& S = reinterpret_cast<SM*>(smem_raw)[warp];
-  const int tl = blockIdx.x * kWarpsPerBlock + warp;
+  const int tl = blockIdx.x * WPB + warp;
   if (tl >= band_tiles) return;
   const int tile = g.ty0 * g.tiles_x + tl;
   const int tx0 = (tile % g.tiles_x) * kTile, ty0 = (tile / g.tiles_x) * kTile;
