@@ -1281,6 +1281,13 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
 //   bilinear: block origin (x0, y0) and, per block corner k = 2 dy + dx,
 //             the weight w_k (pinned fp32, R1/R3)
 //   Gaussian: u, v and the conic; the pixel lane evaluates q and w (R17)
+// One chunk's point records (and unpacked C = 4 features), copied into SMEM
+// with cp.async one chunk ahead of their use: the gathers of chunk k + 1 are
+// in flight while chunk k's pixels are composited, at no register cost.
+struct RecBuf {
+  float4 A[32], B[32], F[32];
+};
+
 template <int CMAX>
 struct ChunkSmem {
   union {
@@ -1303,6 +1310,7 @@ template <int CMAX>
 struct FwdSmem {
   unsigned long long keys[kWarpSortCap];
   ChunkSmem<CMAX> ch;
+  RecBuf rb;
 };
 
 // Backward per-warp SMEM.  The pixel's upstream gradient G is staged per
@@ -1322,6 +1330,7 @@ struct BwdSmem {
   float Gs[64][CMAX];
   float acc[32][kStride];
   int touched[32];
+  RecBuf rb;
 };
 
 // 1/x to ~1 ulp (MUFU.RCP; x in [0.01, 1] here): the backward's T recovery
@@ -1349,6 +1358,34 @@ __device__ __forceinline__ EntryRegs load_entry(const DevCfg& g, const PointRec*
   r.A = __ldg(&rec[idx].a);
   r.B = __ldg(&rec[idx].b);
   if (CMAX == 4 && !packed && g.C == 4) r.F = __ldg(reinterpret_cast<const float4*>(feat) + idx);
+  return r;
+}
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Issue the copies of entry `idx`'s record into slot `lane` (valid lanes only).
+template <int CMAX>
+__device__ __forceinline__ void prefetch_entry(RecBuf& rb, const DevCfg& g, const PointRec* __restrict__ rec,
+                                               const float* __restrict__ feat, bool packed, uint32_t idx,
+                                               bool valid, int lane) {
+  if (valid) {
+    cp_async16(&rb.A[lane], &rec[idx].a);
+    cp_async16(&rb.B[lane], &rec[idx].b);
+    if (CMAX == 4 && !packed && g.C == 4) cp_async16(&rb.F[lane], reinterpret_cast<const float4*>(feat) + idx);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+__device__ __forceinline__ EntryRegs entry_from_buf(const RecBuf& rb, uint32_t idx, int lane) {
+  EntryRegs r;
+  r.idx = idx;
+  r.A = rb.A[lane];
+  r.B = rb.B[lane];
+  r.F = rb.F[lane];
   return r;
 }
 
@@ -1594,18 +1631,22 @@ __global__ void __launch_bounds__(WPB * 32) k_blend_fwd(
   b.done = !inB;
   ChunkSmem<CMAX>& cs = S.ch;
   auto idx_at = [&](uint32_t e) -> uint32_t {
-    return small ? (uint32_t)S.keys[e] : __ldg(sorted_idx + begin + e);
+    return e < n ? (small ? (uint32_t)S.keys[e] : __ldg(sorted_idx + begin + e)) : 0u;
   };
+  uint32_t idx = idx_at(lane);
+  prefetch_entry<CMAX>(S.rb, g, rec, feat, packed, idx, lane < n, lane);
   for (uint32_t base = 0; base < n; base += 32) {
     const uint32_t e = base + lane;
     cs.mask[lane] = 0u;
     cs.mask[lane + 32] = 0u;
+    cp_async_wait_all();
     __syncwarp();
-    if (e < n) {
-      const EntryRegs r = load_entry<CMAX>(g, rec, feat, packed, idx_at(e));
-      stage_entry<MODE, CMAX, false>(cs, lane, g, r, feat, packed, tx0, ty0);
+    if (e < n) stage_entry<MODE, CMAX, false>(cs, lane, g, entry_from_buf(S.rb, idx, lane), feat, packed, tx0, ty0);
+    __syncwarp();
+    if (base + 32 < n) {  // the next chunk's records fly while this one is composited
+      idx = idx_at(e + 32);
+      prefetch_entry<CMAX>(S.rb, g, rec, feat, packed, idx, e + 32 < n, lane);
     }
-    __syncwarp();
     blend_pixel<MODE, CMAX, COUNT>(cs, g, cs.mask[lane], px, pyA, pcA, base, a);
     blend_pixel<MODE, CMAX, COUNT>(cs, g, cs.mask[lane + 32], px, pyB, pcA + 8, base, b);
     __syncwarp();
@@ -1613,6 +1654,7 @@ __global__ void __launch_bounds__(WPB * 32) k_blend_fwd(
   }
   if (inA) write_pixel<CMAX>(cam, g, out, bg, px, pyA, a);
   if (inB) write_pixel<CMAX>(cam, g, out, bg, px, pyB, b);
+  cp_async_wait_all();  // an early exit may leave the next chunk's copies in flight
 }
 
 // ---------------------------------------------------------------- H8
@@ -1779,24 +1821,31 @@ __global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? 28 / WPB : 1) k_blend_bw
   if (tmax == 0) return;
   ChunkSmem<CMAX>& cs = S.ch;
   const int chunk0 = (int)((tmax - 1) >> 5);
-  // the list index of the next chunk is loaded one chunk ahead (one register)
-  uint32_t idx_next = chunk0 * 32 + lane < tmax ? __ldg(sorted_idx + begin + chunk0 * 32 + lane) : 0u;
+  // software pipeline over the chunks (reverse order): the records of the
+  // next chunk are copied into SMEM (cp.async) while this one is processed,
+  // and the list indices are loaded one chunk further ahead
+  uint32_t idx = chunk0 * 32 + lane < tmax ? __ldg(sorted_idx + begin + chunk0 * 32 + lane) : 0u;
+  prefetch_entry<CMAX>(S.rb, g, rec, feat, packed, idx, chunk0 * 32 + lane < tmax, lane);
+  uint32_t idx_next = chunk0 > 0 ? __ldg(sorted_idx + begin + chunk0 * 32 - 32 + lane) : 0u;
   for (int chunk = chunk0; chunk >= 0; --chunk) {
     const uint32_t base = (uint32_t)chunk * 32;
     const uint32_t e = base + lane;
-    const uint32_t idx = idx_next;
-    if (chunk > 0) idx_next = __ldg(sorted_idx + begin + base - 32 + lane);
     cs.mask[lane] = 0u;
     cs.mask[lane + 32] = 0u;
 #pragma unroll
     for (int c = 0; c < SM::kStride; ++c) S.acc[lane][c] = 0.0f;
     S.touched[lane] = 0;
+    cp_async_wait_all();
     __syncwarp();
-    if (e < tmax) {
-      const EntryRegs r = load_entry<CMAX>(g, rec, feat, packed, idx);
-      stage_entry<MODE, CMAX, true>(cs, lane, g, r, feat, packed, tx0, ty0, &S.gw[lane][0], &S.rc[lane][0]);
+    if (e < tmax)
+      stage_entry<MODE, CMAX, true>(cs, lane, g, entry_from_buf(S.rb, idx, lane), feat, packed, tx0, ty0,
+                                    &S.gw[lane][0], &S.rc[lane][0]);
+    __syncwarp();
+    const uint32_t idx_pf = idx_next;  // chunk - 1 (every entry below tmax)
+    if (chunk > 0) {
+      prefetch_entry<CMAX>(S.rb, g, rec, feat, packed, idx_pf, true, lane);
+      if (chunk > 1) idx_next = __ldg(sorted_idx + begin + base - 64 + lane);
     }
-    __syncwarp();
     bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane] & below_mask(a.last, base), px, pyA, pcA, a);
     bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane + 32] & below_mask(b.last, base), px, pyB, pcA + 8, b);
     __syncwarp();
@@ -1833,6 +1882,7 @@ __global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? 28 / WPB : 1) k_blend_bw
       atomicAdd(in.g_op + idx, gsum[CMAX]);
     }
     __syncwarp();
+    idx = idx_pf;
   }
 }
 
