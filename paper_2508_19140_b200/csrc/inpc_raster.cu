@@ -71,6 +71,7 @@ struct inpc_ctx {
   int num_sms = 148;
   int big_grid = 0;
   // scratch (shared by views, stream ordered)
+  Buf scat;  // unfused bilinear binning: depth key + tile block | corner mask per point
   Buf zeroed, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg, g_eval;
   Buf f4_rec, f4_keys, f4_vals, f4_keys2, f4_vals2, f4_hist, f4_scan, f4_misc;  // NEXT f4 baseline
   int bin_grid[3] = {0, 0, 0};  // cooperative grid of k_bin_bilinear<2,4,8>
@@ -168,7 +169,7 @@ struct AllocScope {
 };
 
 void release_all(inpc_ctx* c) {
-  for (Buf* b : {&c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots,
+  for (Buf* b : {&c->scat, &c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots,
                  &c->agg, &c->g_eval, &c->tmp, &c->overflow, &c->f4_rec, &c->f4_keys, &c->f4_vals,
                  &c->f4_keys2, &c->f4_vals2, &c->f4_hist, &c->f4_scan, &c->f4_misc})
     free_buf(*b);
@@ -291,16 +292,16 @@ void set_smem(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <int MODE, int CMAX, bool COUNT, int WPB>
+template <int MODE, int CMAX, bool COUNT, int WPB, bool PF>
 void launch_blend_fwd_w(int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
                         const PointRec* rec, const float* feat, bool packed, const float* bg,
                         const uint32_t* ranges, const unsigned long long* entries,
                         uint32_t* sorted_idx, const BlendOut& o) {
-  const size_t smem = WPB * sizeof(FwdSmem<CMAX>);
-  static bool once = (set_smem(k_blend_fwd<MODE, CMAX, COUNT, WPB>, smem), true);
+  const size_t smem = WPB * sizeof(FwdSmem<CMAX, PF>);
+  static bool once = (set_smem(k_blend_fwd<MODE, CMAX, COUNT, WPB, PF>, smem), true);
   (void)once;
   const int grid = (band_tiles + WPB - 1) / WPB;
-  k_blend_fwd<MODE, CMAX, COUNT, WPB><<<grid, WPB * 32, smem, s>>>(
+  k_blend_fwd<MODE, CMAX, COUNT, WPB, PF><<<grid, WPB * 32, smem, s>>>(
       dc, g, band_tiles, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
 }
 
@@ -309,32 +310,37 @@ int env_wpb(const char* name) {
   return e ? atoi(e) : kWarpsPerBlock;
 }
 
+// record prefetch in the forward (PF) below this many input points per tile
+constexpr int64_t kFwdPrefetchMaxDensity = 512;
+
 template <int MODE, int CMAX, bool COUNT>
 void launch_blend_fwd_t(int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
                         const PointRec* rec, const float* feat, bool packed, const float* bg,
                         const uint32_t* ranges, const unsigned long long* entries,
-                        uint32_t* sorted_idx, const BlendOut& o) {
+                        uint32_t* sorted_idx, const BlendOut& o, bool pf) {
 #ifdef INPC_FAST_BUILD
   static const int w = env_wpb("INPC_WPB_FWD");
-  if (w == 1) return launch_blend_fwd_w<MODE, CMAX, COUNT, 1>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
-  if (w == 2) return launch_blend_fwd_w<MODE, CMAX, COUNT, 2>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
-  if (w == 8) return launch_blend_fwd_w<MODE, CMAX, COUNT, 8>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
+  if (w == 1) return launch_blend_fwd_w<MODE, CMAX, COUNT, 1, false>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
+  if (w == 2) return launch_blend_fwd_w<MODE, CMAX, COUNT, 2, false>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
 #endif
-  launch_blend_fwd_w<MODE, CMAX, COUNT, kWarpsPerBlock>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
+  if (CMAX == 4 && pf)
+    launch_blend_fwd_w<MODE, CMAX, COUNT, kWarpsPerBlock, CMAX == 4>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
+  else
+    launch_blend_fwd_w<MODE, CMAX, COUNT, kWarpsPerBlock, false>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries, sorted_idx, o);
 }
 
 template <int MODE, int CMAX>
 void launch_blend_fwd(int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
                       const PointRec* rec, const float* feat, bool packed, const float* bg,
                       const uint32_t* ranges, const unsigned long long* entries,
-                      uint32_t* sorted_idx, const BlendOut& o) {
+                      uint32_t* sorted_idx, const BlendOut& o, bool pf) {
   // the debug counts (n_frag, n_contrib) need every fragment visited
   if (o.nfrag || o.ncontrib)
     launch_blend_fwd_t<MODE, CMAX, true>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries,
-                                         sorted_idx, o);
+                                         sorted_idx, o, pf);
   else
     launch_blend_fwd_t<MODE, CMAX, false>(band_tiles, s, dc, g, rec, feat, packed, bg, ranges, entries,
-                                          sorted_idx, o);
+                                          sorted_idx, o, pf);
 }
 
 template <int MODE, int CMAX, int WPB>
@@ -365,16 +371,16 @@ template <int MODE>
 void dispatch_blend_fwd(int cmax, int band_tiles, cudaStream_t s, const DevCam& dc, const DevCfg& g,
                         const PointRec* xyz, const float* feat, bool op, const float* bg,
                         const uint32_t* ranges, const unsigned long long* entries,
-                        uint32_t* sorted_idx, const BlendOut& o) {
+                        uint32_t* sorted_idx, const BlendOut& o, bool pf) {
   switch (cmax) {
-    case 4: launch_blend_fwd<MODE, 4>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    case 4: launch_blend_fwd<MODE, 4>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o, pf); break;
 #ifndef INPC_FAST_BUILD  // diagnostics build: C <= 4 kernels only
-    case 8: launch_blend_fwd<MODE, 8>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
-    case 16: launch_blend_fwd<MODE, 16>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
-    case 32: launch_blend_fwd<MODE, 32>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
-    default: launch_blend_fwd<MODE, 64>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    case 8: launch_blend_fwd<MODE, 8>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o, pf); break;
+    case 16: launch_blend_fwd<MODE, 16>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o, pf); break;
+    case 32: launch_blend_fwd<MODE, 32>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o, pf); break;
+    default: launch_blend_fwd<MODE, 64>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o, pf); break;
 #else
-    default: launch_blend_fwd<MODE, 4>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o); break;
+    default: launch_blend_fwd<MODE, 4>(band_tiles, s, dc, g, xyz, feat, op, bg, ranges, entries, sorted_idx, o, pf); break;
 #endif
   }
 }
@@ -696,22 +702,27 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       }
 #endif
     }
+    uint2* scp = nullptr;  // bilinear: compact per-point scatter data (tile block + mask in 32 bits)
+    if (N > 0 && !fused_kp && !gauss && T < (1 << 28)) {
+      if ((st = ensure(c->scat, (size_t)N * 8, s))) return st;
+      scp = (uint2*)c->scat.p;
+    }
     if (N > 0 && !fused_kp) {
       StageTimer tm(c, s, kStProject, 1);
       PointRec* recp = (PointRec*)vs.rec.p;
       uint4* slp = (uint4*)c->slots.p;
       if (gauss && sh)
         k_project_count<1, true><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N, recp,
-                                                                 tc, nullptr, dk, dt, feat_out);
+                                                                 tc, nullptr, dk, dt, feat_out, nullptr);
       else if (gauss)
         k_project_count<1, false><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N, recp,
-                                                                  tc, nullptr, dk, dt, feat_out);
+                                                                  tc, nullptr, dk, dt, feat_out, nullptr);
       else if (sh)
         k_project_count<0, true><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N, recp,
-                                                                 tc, slp, dk, dt, feat_out);
+                                                                 tc, slp, dk, dt, feat_out, scp);
       else
         k_project_count<0, false><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N, recp,
-                                                                  tc, slp, dk, dt, feat_out);
+                                                                  tc, slp, dk, dt, feat_out, scp);
       CK(cudaGetLastError());
     }
     if (!fused_kp) {
@@ -746,7 +757,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
         k_scatter_slots<<<nblk, kPointThreads, 0, s>>>(g, (const PointRec*)vs.rec.p,
                                                        (const uint4*)c->slots.p, N,
                                                        (const uint32_t*)vs.ranges.p,
-                                                       (unsigned long long*)c->entries.p);
+                                                       (unsigned long long*)c->entries.p, scp);
       CK(cudaGetLastError());
     }
     if (N > kWarpSortCap && !fused_kp) {  // a tile can only exceed the cap with > cap points
@@ -773,14 +784,15 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       o.ncontrib = out_ncontrib ? out_ncontrib + (size_t)v * P : nullptr;
       o.T_final = (float*)vs.T_final.p;
       o.last = (uint32_t*)vs.last.p;
+      const bool pf = N < kFwdPrefetchMaxDensity * (int64_t)T;
       if (gauss)
         dispatch_blend_fwd<1>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_blend, false, bg_v,
                               (const uint32_t*)vs.ranges.p, (const unsigned long long*)c->entries.p,
-                              (uint32_t*)vs.sorted_idx.p, o);
+                              (uint32_t*)vs.sorted_idx.p, o, pf);
       else
         dispatch_blend_fwd<0>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_blend, packed, bg_v,
                               (const uint32_t*)vs.ranges.p, (const unsigned long long*)c->entries.p,
-                              (uint32_t*)vs.sorted_idx.p, o);
+                              (uint32_t*)vs.sorted_idx.p, o, pf);
       CK(cudaGetLastError());
     }
   }
@@ -955,7 +967,7 @@ int inpc_sort_single64(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     const int nblk = (int)((N + (int64_t)kPointThreads * kPPT - 1) / ((int64_t)kPointThreads * kPPT));
     k_project_count<0, false><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, nullptr, false, N,
                                                               (PointRec*)c->f4_rec.p, nullptr, nullptr,
-                                                              nullptr, nullptr, nullptr);
+                                                              nullptr, nullptr, nullptr, nullptr);
     CK(cudaGetLastError());
   }
   unsigned long long* ka = (unsigned long long*)c->f4_keys.p;

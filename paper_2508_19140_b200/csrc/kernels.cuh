@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
     DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ opacity,
     const float* __restrict__ feat, bool pack, int64_t N, PointRec* __restrict__ rec,
     uint32_t* __restrict__ tile_count, uint4* __restrict__ slots, uint32_t* __restrict__ dbg_key,
-    uint32_t* __restrict__ dbg_tiles, float* __restrict__ feat_out) {
+    uint32_t* __restrict__ dbg_tiles, float* __restrict__ feat_out, uint2* __restrict__ scat) {
   const int64_t stride = (int64_t)gridDim.x * kPointThreads;
   const int64_t i0 = (int64_t)blockIdx.x * kPointThreads + threadIdx.x;
   float X[kPPT], Y[kPPT], Z[kPPT], O[kPPT];
@@ -178,7 +178,10 @@ __global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
                                      (f.yhi / kTile - f.ylo / kTile + 1))
                         : 0u;
     }
-    if (!ok || !tile_count) continue;  // tile_count null: records only (f4 baseline)
+    if (!ok || !tile_count) {  // tile_count null: records only (f4 baseline)
+      if (MODE == 0 && scat) scat[i] = make_uint2(0u, 0u);
+      continue;
+    }
     int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
     int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
     if (MODE == 0) {
@@ -194,6 +197,12 @@ __global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
                                              : 0xFFFFFFFFu;
       }
       slots[i] = make_uint4(sl[0], sl[1], sl[2], sl[3]);
+      if (scat) {  // what the scatter needs, in 8 bytes: depth key, tile block | corner mask << 28
+        uint32_t vm = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) vm |= (sl[c] != 0xFFFFFFFFu ? 1u : 0u) << c;
+        scat[i] = make_uint2(__float_as_uint(p.zc), (uint32_t)(ty_lo * g.tiles_x + tx_lo) | (vm << 28));
+      }
     } else {
       for (int ty = ty_lo; ty <= ty_hi; ++ty)
         for (int tx = tx_lo; tx <= tx_hi; ++tx) atomicAdd(tile_count + (size_t)ty * g.tiles_x + tx, 1u);
@@ -378,9 +387,32 @@ __global__ void __launch_bounds__(kPointThreads) k_scatter(
 // ranges[tile_k] + slot_k, the slot taken in k_project_count.
 __global__ void __launch_bounds__(kPointThreads) k_scatter_slots(
     DevCfg g, const PointRec* __restrict__ rec, const uint4* __restrict__ slots, int64_t N,
-    const uint32_t* __restrict__ ranges, unsigned long long* __restrict__ entries) {
+    const uint32_t* __restrict__ ranges, unsigned long long* __restrict__ entries,
+    const uint2* __restrict__ scat) {
   const int64_t stride = (int64_t)gridDim.x * kPointThreads;
   const int64_t i0 = (int64_t)blockIdx.x * kPointThreads + threadIdx.x;
+  if (scat) {  // 8 bytes per point (+ 16 per visible point) instead of the 32-byte record
+    uint2 q[kPPT];
+#pragma unroll
+    for (int k = 0; k < kPPT; ++k) {
+      int64_t i = i0 + k * stride;
+      q[k] = i < N ? __ldg(scat + i) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < kPPT; ++k) {
+      int64_t i = i0 + k * stride;
+      if (!q[k].x) continue;
+      const uint4 s4 = __ldg(slots + i);
+      const uint32_t sl[4] = {s4.x, s4.y, s4.z, s4.w};
+      const unsigned long long kv = ((unsigned long long)q[k].x << 32) | (uint32_t)i;
+      const uint32_t t0 = q[k].y & 0x0FFFFFFFu;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if ((q[k].y >> (28 + c)) & 1u)
+          entries[__ldg(ranges + t0 + (uint32_t)(c & 1) + (uint32_t)(c >> 1) * g.tiles_x) + sl[c]] = kv;
+    }
+    return;
+  }
   float4 A[kPPT];
 #pragma unroll
   for (int k = 0; k < kPPT; ++k) {
@@ -1284,9 +1316,11 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
 // One chunk's point records (and unpacked C = 4 features), copied into SMEM
 // with cp.async one chunk ahead of their use: the gathers of chunk k + 1 are
 // in flight while chunk k's pixels are composited, at no register cost.
-struct RecBuf {
-  float4 A[32], B[32], F[32];
+template <int NS>
+struct RecBufT {
+  float4 A[NS], B[NS], F[NS];
 };
+using RecBuf = RecBufT<32>;
 
 template <int CMAX>
 struct ChunkSmem {
@@ -1306,11 +1340,19 @@ struct ChunkSmem {
   uint32_t idx[32];
 };
 
-template <int CMAX>
+template <int CMAX, bool PF = false>
 struct FwdSmem {
   unsigned long long keys[kWarpSortCap];
   ChunkSmem<CMAX> ch;
   RecBuf rb;
+};
+// without the record prefetch the SMEM footprint stays small (a larger L1
+// carveout: measured 508 vs 731 us on cfg 4)
+template <int CMAX>
+struct FwdSmem<CMAX, false> {
+  unsigned long long keys[kWarpSortCap];
+  ChunkSmem<CMAX> ch;
+  RecBufT<1> rb;  // unused
 };
 
 // Backward per-warp SMEM.  The pixel's upstream gradient G is staged per
@@ -1368,8 +1410,8 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Issue the copies of entry `idx`'s record into slot `lane` (valid lanes only).
-template <int CMAX>
-__device__ __forceinline__ void prefetch_entry(RecBuf& rb, const DevCfg& g, const PointRec* __restrict__ rec,
+template <int CMAX, typename RB>
+__device__ __forceinline__ void prefetch_entry(RB& rb, const DevCfg& g, const PointRec* __restrict__ rec,
                                                const float* __restrict__ feat, bool packed, uint32_t idx,
                                                bool valid, int lane) {
   if (valid) {
@@ -1380,7 +1422,8 @@ __device__ __forceinline__ void prefetch_entry(RecBuf& rb, const DevCfg& g, cons
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-__device__ __forceinline__ EntryRegs entry_from_buf(const RecBuf& rb, uint32_t idx, int lane) {
+template <typename RB>
+__device__ __forceinline__ EntryRegs entry_from_buf(const RB& rb, uint32_t idx, int lane) {
   EntryRegs r;
   r.idx = idx;
   r.A = rb.A[lane];
@@ -1597,7 +1640,13 @@ __device__ __forceinline__ void write_pixel(const DevCam& cam, const DevCfg& g, 
 
 // ---------------------------------------------------------------- H4/H6 (small tiles) + H7
 // One warp per 8x8 tile; lane l owns pixels (l & 7, l >> 3) and (l & 7, 4 + (l >> 3)).
-template <int MODE, int CMAX, bool COUNT, int WPB = kWarpsPerBlock>
+// PF: records of the next chunk copied into SMEM (cp.async) while this one is
+// composited, for tiles whose list fits the warp sort.  Chosen by the host
+// from the cloud density (measured: cfg 3 fwd 261 -> 244 us, cfg 5 16.3 ->
+// 14.6 ms per 64 views, cfg 2 neutral; cfg 4 (~1000 points per tile, long
+// lists ended by early termination) 514 -> 780 us, so dense clouds run
+// without).
+template <int MODE, int CMAX, bool COUNT, int WPB = kWarpsPerBlock, bool PF = false>
 __global__ void __launch_bounds__(WPB * 32) k_blend_fwd(
     DevCam cam, DevCfg g, int band_tiles, const PointRec* __restrict__ rec,
     const float* __restrict__ feat, bool packed, const float* __restrict__ bg,
@@ -1605,7 +1654,7 @@ __global__ void __launch_bounds__(WPB * 32) k_blend_fwd(
     uint32_t* __restrict__ sorted_idx, BlendOut out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  FwdSmem<CMAX>& S = reinterpret_cast<FwdSmem<CMAX>*>(smem_raw)[warp];
+  FwdSmem<CMAX, PF>& S = reinterpret_cast<FwdSmem<CMAX, PF>*>(smem_raw)[warp];
   const int tl = blockIdx.x * WPB + warp;
   if (tl >= band_tiles) return;  // warp-uniform; no block barriers below
   const int tile = g.ty0 * g.tiles_x + tl;
@@ -1633,17 +1682,22 @@ __global__ void __launch_bounds__(WPB * 32) k_blend_fwd(
   auto idx_at = [&](uint32_t e) -> uint32_t {
     return e < n ? (small ? (uint32_t)S.keys[e] : __ldg(sorted_idx + begin + e)) : 0u;
   };
+  constexpr bool pf = PF;
   uint32_t idx = idx_at(lane);
-  prefetch_entry<CMAX>(S.rb, g, rec, feat, packed, idx, lane < n, lane);
+  if (pf) prefetch_entry<CMAX>(S.rb, g, rec, feat, packed, idx, lane < n, lane);
   for (uint32_t base = 0; base < n; base += 32) {
     const uint32_t e = base + lane;
     cs.mask[lane] = 0u;
     cs.mask[lane + 32] = 0u;
-    cp_async_wait_all();
+    if (pf) cp_async_wait_all();
     __syncwarp();
-    if (e < n) stage_entry<MODE, CMAX, false>(cs, lane, g, entry_from_buf(S.rb, idx, lane), feat, packed, tx0, ty0);
+    if (e < n) {
+      const EntryRegs r = pf ? entry_from_buf(S.rb, idx, lane)
+                             : load_entry<CMAX>(g, rec, feat, packed, idx_at(e));
+      stage_entry<MODE, CMAX, false>(cs, lane, g, r, feat, packed, tx0, ty0);
+    }
     __syncwarp();
-    if (base + 32 < n) {  // the next chunk's records fly while this one is composited
+    if (pf && base + 32 < n) {  // the next chunk's records fly while this one is composited
       idx = idx_at(e + 32);
       prefetch_entry<CMAX>(S.rb, g, rec, feat, packed, idx, e + 32 < n, lane);
     }
@@ -1654,7 +1708,7 @@ __global__ void __launch_bounds__(WPB * 32) k_blend_fwd(
   }
   if (inA) write_pixel<CMAX>(cam, g, out, bg, px, pyA, a);
   if (inB) write_pixel<CMAX>(cam, g, out, bg, px, pyB, b);
-  cp_async_wait_all();  // an early exit may leave the next chunk's copies in flight
+  if (PF) cp_async_wait_all();  // an early exit may leave the next chunk's copies in flight
 }
 
 // ---------------------------------------------------------------- H8
