@@ -1,3 +1,4 @@
+#!/bin/bash
 # three-way: head (A), mid (M), in-tree (B); bench stage times for $CFG
 L=paper_2508_19140_b200/libinpc_raster.so
 cp $L /tmp/new.so

@@ -1,3 +1,4 @@
+#!/bin/bash
 L=paper_2508_19140_b200/libinpc_raster.so
 cp $L /tmp/new.so
 for v in A M; do
