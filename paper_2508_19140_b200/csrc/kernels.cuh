@@ -1371,7 +1371,6 @@ struct BwdSmem {
   float rc[32][4];   // bilinear 1 / (1 - alpha) per corner (approximate: the recovery adds a Newton step)
   float Gs[64][CMAX];
   float acc[32][kStride];
-  int touched[32];
   RecBuf rb;
 };
 
@@ -1488,10 +1487,14 @@ __device__ __forceinline__ void stage_entry(ChunkSmem<CMAX>& cs, int lane, const
   const int yl = max(f.ylo, ty0) - ty0, yh = min(f.yhi, ty0 + kTile - 1) - ty0;
   if (MODE == 0) {  // the 2x2 block: four predicated marks, no loops
     const int bx = f.x0 - tx0, by = f.y0 - ty0;
+    // SKIP_ZERO_ALPHA_GRAD (A/B of the original INPC behaviour): the
+    // backward leaves alpha = 0 fragments out of its masks
+    const bool skipz = BWD && (g.flags & kFlagSkipZero);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int xx = bx + (k & 1), yy = by + (k >> 1);
-      if (xx >= xl && xx <= xh && yy >= yl && yy <= yh) atomicOr(&cs.mask[yy * kTile + xx], 1u << lane);
+      if (xx >= xl && xx <= xh && yy >= yl && yy <= yh && !(skipz && cs.ac[lane][k] == 0.0f))
+        atomicOr(&cs.mask[yy * kTile + xx], 1u << lane);
     }
   } else {
     for (int yy = yl; yy <= yh; ++yy)
@@ -1803,8 +1806,8 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
       one_m = __fsub_rn(1.0f, alpha);
       rcp = __frcp_rn(one_m);
       z = cs.z[e];
+      if ((g.flags & kFlagSkipZero) && alpha == 0.0f) continue;
     }
-    if ((g.flags & kFlagSkipZero) && alpha == 0.0f) continue;
     // T_k = T_{k+1} / (1 - alpha_k) from the staged reciprocal plus one
     // Newton correction of the residual (as accurate as the IEEE division on
     // 0 <= alpha < 1, without its special-case branch).  The recovery error
@@ -1826,13 +1829,11 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
     if (SM::kSlots) {
       S.acc[e][2 * corner] = ta;  // odd row stride: scalar stores
       S.acc[e][2 * corner + 1] = go;
-      S.touched[e] = 1;
     } else {
 #pragma unroll
       for (int c = 0; c < CMAX; ++c)
         if (c < g.C) atomicAdd(&S.acc[e][c], ta * s.G[c]);
       atomicAdd(&S.acc[e][CMAX], go);
-      S.touched[e] = 1;
     }
     s.S = alpha * gf + one_m * s.S;
     s.SD = alpha * z + one_m * s.SD;
@@ -1888,7 +1889,6 @@ __global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? 28 / WPB : 1) k_blend_bw
     cs.mask[lane + 32] = 0u;
 #pragma unroll
     for (int c = 0; c < SM::kStride; ++c) S.acc[lane][c] = 0.0f;
-    S.touched[lane] = 0;
     cp_async_wait_all();
     __syncwarp();
     if (e < tmax)
@@ -1903,7 +1903,7 @@ __global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? 28 / WPB : 1) k_blend_bw
     bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane] & below_mask(a.last, base), px, pyA, pcA, a);
     bwd_pixel<MODE, CMAX>(S, g, cs.mask[lane + 32] & below_mask(b.last, base), px, pyB, pcA + 8, b);
     __syncwarp();
-    if (e < tmax && S.touched[lane]) {
+    if (e < tmax) {  // entries without a contribution (all sums zero) send nothing
       float gsum[CMAX + 1];
 #pragma unroll
       for (int c = 0; c <= CMAX; ++c) gsum[c] = 0.0f;
@@ -1925,15 +1925,20 @@ __global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? 28 / WPB : 1) k_blend_bw
 #pragma unroll
         for (int c = 0; c <= CMAX; ++c) gsum[c] = S.acc[lane][c];
       }
-      if (CMAX == 4 && g.C == 4) {
-        atomicAdd(reinterpret_cast<float4*>(in.g_feat) + idx,
-                  make_float4(gsum[0], gsum[1], gsum[2], gsum[3]));
-      } else {
+      bool nz = false;
 #pragma unroll
-        for (int c = 0; c < CMAX; ++c)
-          if (c < g.C) atomicAdd(in.g_feat + (size_t)idx * g.C + c, gsum[c]);
+      for (int c = 0; c <= CMAX; ++c) nz |= gsum[c] != 0.0f;
+      if (nz) {
+        if (CMAX == 4 && g.C == 4) {
+          atomicAdd(reinterpret_cast<float4*>(in.g_feat) + idx,
+                    make_float4(gsum[0], gsum[1], gsum[2], gsum[3]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < CMAX; ++c)
+            if (c < g.C) atomicAdd(in.g_feat + (size_t)idx * g.C + c, gsum[c]);
+        }
+        atomicAdd(in.g_op + idx, gsum[CMAX]);
       }
-      atomicAdd(in.g_op + idx, gsum[CMAX]);
     }
     __syncwarp();
     idx = idx_pf;
