@@ -726,9 +726,14 @@ constexpr int kRadixItems = 8;
 constexpr int kRadixMinN = 2048;  // smaller chunks: the bitonic network is cheaper than the passes
 constexpr bool kUseRadix = true;  // chunks > kRadixMinN: radix (cfg 4: 1.15 ms vs 1.48 ms with 32-bit bitonic chunks)
 constexpr int kRadixMaxRun = 64;
+#ifndef INPC_BUCKET_MIN_N
+#define INPC_BUCKET_MIN_N 1024  // smaller chunks: the 32-bit bitonic network is cheaper (cfg 5)
+#endif
+constexpr int kBucketMinN = INPC_BUCKET_MIN_N;  // k_sort_big chunks above this: bucket sort first
 constexpr int kRadixStride = 257;  // hist row stride (digit-major scan reads are conflict-free)
 constexpr int kRadixSmemU32 = 32 * kRadixStride + 32 + 4;
 __device__ __forceinline__ bool block_radix_depth(unsigned long long* s, int n, uint32_t* sm);
+template <int BITS>
 __device__ __forceinline__ bool block_bucket_sort(unsigned long long* s, int n, uint32_t* sm);
 __device__ __forceinline__ bool block_sort32_depth(const unsigned long long* s, int n, int np, uint32_t* u,
                                                    uint32_t* misc);
@@ -806,10 +811,12 @@ __device__ __forceinline__ void big_sort_body(
     bool sorted = false, perm = false;
     uint32_t* u = radix_smem;                                  // 32-bit keys / permutation
     uint32_t* misc = radix_smem ? radix_smem + 32 * kRadixStride + 32 : nullptr;
-    if (radix_smem && kUseRadix && n > (uint32_t)kRadixMinN) {
+    if (radix_smem && n > (uint32_t)kBucketMinN) {
       for (int k = threadIdx.x; k < (int)n; k += blockDim.x) s[k] = entries[begin + k];
       __syncthreads();
-      sorted = block_bucket_sort(s, (int)n, radix_smem) || block_radix_depth(s, (int)n, radix_smem);
+      // about 4 buckets per key
+      sorted = n > 2048u ? block_bucket_sort<14>(s, (int)n, radix_smem) : block_bucket_sort<13>(s, (int)n, radix_smem);
+      if (!sorted && kUseRadix && n > (uint32_t)kRadixMinN) sorted = block_radix_depth(s, (int)n, radix_smem);
     } else if (radix_smem) {
       for (int k = threadIdx.x; k < (int)n; k += blockDim.x) s[k] = entries[begin + k];
       __syncthreads();
@@ -901,6 +908,7 @@ constexpr int kBucketMax = 64;
 static_assert(kBuckets / 2 + 36 <= kRadixSmemU32, "bucket sort scratch");
 static_assert(kBigChunkLarge < 65536, "16-bit bucket counters");
 
+template <int BITS>
 __device__ __forceinline__ bool block_bucket_sort(unsigned long long* s, int n, uint32_t* sm) {
   // pos: bucket b's 16-bit counter / offset / cursor is half (b & 1) of word b >> 1
   uint32_t* pos = sm;                      // [kBuckets / 2]
@@ -908,14 +916,16 @@ __device__ __forceinline__ bool block_bucket_sort(unsigned long long* s, int n, 
   auto half = [](uint32_t word, uint32_t b) { return (b & 1u) ? word >> 16 : word & 0xFFFFu; };
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   constexpr int kItems = kBigChunkLarge / kBigThreadsLarge;
-  constexpr int kPer = kBuckets / kBigThreadsLarge;  // buckets per thread in the scan
+  constexpr int kPer = (1 << BITS) / kBigThreadsLarge;  // buckets per thread in the scan
   uint32_t o = 0u, a = 0xFFFFFFFFu;
   for (int i = tid; i < n; i += kBigThreadsLarge) {
     const uint32_t d = (uint32_t)(s[i] >> 32);
     o |= d;
     a &= d;
   }
-  for (int b = tid; b < kBuckets / 2; b += kBigThreadsLarge) pos[b] = 0u;
+  static_assert(BITS >= 11 && BITS <= kBucketBits, "bucket bits");
+  constexpr int bits = BITS, nbk = 1 << BITS, per = nbk / kBigThreadsLarge;
+  for (int b = tid; b < nbk / 2; b += kBigThreadsLarge) pos[b] = 0u;
   if (tid == 0) {
     misc[0] = 0u;
     misc[1] = 0xFFFFFFFFu;
@@ -932,8 +942,8 @@ __device__ __forceinline__ bool block_bucket_sort(unsigned long long* s, int n, 
   const uint32_t vary = misc[0] ^ misc[1];
   if (vary == 0u) return false;  // one depth: index order only (radix run fix-up / bitonic)
   const int hi = 31 - __clz(vary);
-  const int sh = hi >= kBucketBits - 1 ? hi - (kBucketBits - 1) : 0;  // bits above hi are equal
-  auto digit = [&](unsigned long long k) { return (uint32_t)(k >> (32 + sh)) & (kBuckets - 1u); };
+  const int sh = hi >= bits - 1 ? hi - (bits - 1) : 0;  // bits above hi are equal
+  auto digit = [&](unsigned long long k) { return (uint32_t)(k >> (32 + sh)) & (uint32_t)(nbk - 1); };
   unsigned long long kv[kItems];  // the chunk's keys, held across the count and the scatter
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
@@ -945,12 +955,12 @@ __device__ __forceinline__ bool block_bucket_sort(unsigned long long* s, int n, 
     }
   }
   __syncthreads();
-  {  // exclusive scan of the counts: thread t owns buckets kPer t .. kPer t + kPer - 1
+  {  // exclusive scan of the counts: thread t owns buckets per t .. per t + per - 1
     uint32_t c[kPer], sum = 0u;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
-      const uint32_t b = kPer * tid + k;
-      c[k] = half(pos[b >> 1], b);
+      const uint32_t b = per * tid + k;
+      c[k] = k < per ? half(pos[b >> 1], b) : 0u;
       sum += c[k];
     }
     uint32_t x = sum;
@@ -973,8 +983,8 @@ __device__ __forceinline__ bool block_bucket_sort(unsigned long long* s, int n, 
     __syncthreads();
     uint32_t run = (w ? misc[4 + w - 1] : 0u) + x - sum;
 #pragma unroll
-    for (int k = 0; k < kPer; k += 2) {  // kPer even: whole words per thread
-      pos[(kPer * tid + k) >> 1] = run | ((run + c[k]) << 16);
+    for (int k = 0; k < kPer; k += 2) {  // per even: whole words per thread
+      if (k < per) pos[(per * tid + k) >> 1] = run | ((run + c[k]) << 16);
       run += c[k] + c[k + 1];
     }
   }
@@ -988,7 +998,7 @@ __device__ __forceinline__ bool block_bucket_sort(unsigned long long* s, int n, 
   __syncthreads();
   // pos[b] is now the end of bucket b, pos[b - 1] its start
   bool bad = false;
-  for (int b = tid; b < kBuckets; b += kBigThreadsLarge) {
+  for (int b = tid; b < nbk; b += kBigThreadsLarge) {
     const int lo = b ? (int)half(pos[(b - 1) >> 1], b - 1) : 0, hi2 = (int)half(pos[b >> 1], b);
     if (hi2 - lo > kBucketMax) {
       bad = true;
