@@ -1501,12 +1501,14 @@ struct FwdSmem<CMAX, false> {
 template <int MODE, int CMAX>
 struct BwdSmem {
   static constexpr bool kSlots = MODE == 0;
-  static constexpr int kStride = kSlots ? 9 : CMAX + 2;  // odd: no bank conflicts
+  // bilinear: 8 floats per entry (4 corners x {T alpha, dL/do}) + pad, rows
+  // 8-byte aligned for one 64-bit store per fragment; Gaussian: odd stride
+  static constexpr int kStride = kSlots ? 10 : CMAX + 2;
   ChunkSmem<CMAX> ch;
   float gw[32][4];   // bilinear dalpha/do per corner: w, or 0 where clamped
   float rc[32][4];   // bilinear 1 / (1 - alpha) per corner (approximate: the recovery adds a Newton step)
   float Gs[64][CMAX];
-  float acc[32][kStride];
+  __align__(8) float acc[32][kStride];
   RecBuf rb;
 };
 
@@ -1963,8 +1965,7 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
     const float ta = Tk * alpha;
     const float go = gw * dA;  // dalpha/do = w, or 0 where the clamp is active
     if (SM::kSlots) {
-      S.acc[e][2 * corner] = ta;  // odd row stride: scalar stores
-      S.acc[e][2 * corner + 1] = go;
+      *reinterpret_cast<float2*>(&S.acc[e][2 * corner]) = make_float2(ta, go);
     } else {
 #pragma unroll
       for (int c = 0; c < CMAX; ++c)
@@ -2051,7 +2052,7 @@ __global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? 28 / WPB : 1) k_blend_bw
         for (int k = 0; k < 4; ++k) {
           const int cx = lx + (k & 1), cy = ly + (k >> 1);
           if (cx < 0 || cx >= kTile || cy < 0 || cy >= kTile) continue;
-          const float2 sl = make_float2(S.acc[lane][2 * k], S.acc[lane][2 * k + 1]);
+          const float2 sl = *reinterpret_cast<const float2*>(&S.acc[lane][2 * k]);
           const float* Gp = &S.Gs[cy * kTile + cx][0];
 #pragma unroll
           for (int c = 0; c < CMAX; ++c) gsum[c] += sl.x * Gp[c];
