@@ -726,6 +726,9 @@ constexpr int kRadixItems = 8;
 constexpr int kRadixMinN = 2048;  // smaller chunks: the bitonic network is cheaper than the passes
 constexpr bool kUseRadix = true;  // chunks > kRadixMinN: radix (cfg 4: 1.15 ms vs 1.48 ms with 32-bit bitonic chunks)
 constexpr int kRadixMaxRun = 64;
+#ifndef INPC_SORT_BIG_MINB
+#define INPC_SORT_BIG_MINB 2  // k_sort_big CTAs per SM (32 registers)
+#endif
 #ifndef INPC_BUCKET_MIN_N
 #define INPC_BUCKET_MIN_N 1024  // smaller chunks: the 32-bit bitonic network is cheaper (cfg 5)
 #endif
@@ -1218,7 +1221,7 @@ __device__ __forceinline__ bool block_sort32_depth(const unsigned long long* s, 
 // 64 KB of dynamic SMEM (+ the radix counters), so tiles up to 8192 entries
 // (cfg 4: 7750 tiles of 2-7k entries) sort in one chunk without merge passes;
 // chunks are sorted by block_radix_depth (bitonic fallback on long ties).
-__global__ void __launch_bounds__(kBigThreadsLarge, 2) k_sort_big(
+__global__ void __launch_bounds__(kBigThreadsLarge, INPC_SORT_BIG_MINB) k_sort_big(
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles,
     uint32_t* big_elem, uint32_t* big_chunk, ViewScalars* sc,
     unsigned long long* entries, unsigned long long* tmp, uint32_t* __restrict__ sorted_idx) {
