@@ -3,23 +3,30 @@
 frames/s and Mpoints/s at 1080p fwd+bwd, % of B200 HBM roofline, 1/2/4/8 GPUs).
 
 One step = one pass of the whole hot path (H1-H8) over one
-synthetic frame: forward (project, tile lists, blend) + backward, with the
-point cloud and upstream gradients resident in HBM.  Default workload =
-config 2 (configs[1]: 2^20-point view-specific cloud, 1920x1080, bilinear,
-fwd+bwd).  Under torchrun (N > 1) every rank renders its own view-specific
-cloud (independent problems, no data-path collective): weak scaling.
+batch of synthetic input, with the point cloud and upstream gradients
+resident in HBM.  Default workload = the north-star configuration
+(BASELINE.json configs[4], SURVEY §8(d) cfg 5): a training-style batch of 64
+1080p camera views of one static 2^23-point cloud with shared features,
+forward + backward, the 64 views split over the ranks, the per-rank gradient
+sums all-reduced in one NCCL call inside the timed step (strong scaling).
+The static cloud is put in spatial (Morton) order once, untimed, by the
+library's inpc_spatial_order; its cost is reported.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 2|3|4|5] [--variant base|sh|env|sh+env]
 
-`--impl reference` times the CPU oracle (oracle/, the only reference this
-paper-only build has) on the host cores, on a bounded sample of the same
-workload, and prints the same JSON line with "impl": "reference".
+`--gpus N` without torchrun's WORLD_SIZE re-launches itself under
+`torch.distributed.run` with N ranks (127.0.0.1).  `--impl reference` times
+the CPU oracle (oracle/, the only reference this paper-only build has) on
+whole views of the same workload and prints the same JSON line with
+"impl": "reference".
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import sys
 import threading
 import time
@@ -32,11 +39,14 @@ sys.path.insert(0, ROOT)
 import synthgen  # noqa: E402
 
 METRIC = "frames/s and Mpoints/s at 1080p fwd+bwd, % of B200 HBM roofline, 1/2/4/8 GPUs"
-WORKLOAD = "cfg2: 2^20-point view-specific cloud, 1920x1080, C=4, bilinear 2x2 splats, fwd+bwd"
-WORKLOAD3 = "cfg3: 4x2^20 ring-buffer cloud, 1920x1080, C=4, Gaussian splats (auto sigma, dilation 0.16), forward only"
-WORKLOAD4 = "cfg4: 2^25-point global extracted cloud, 1920x1080, C=4, bilinear, forward only"
-WORKLOAD5 = "cfg5: 64 orbit views of a 2^23-point cloud, 1920x1080, C=4, bilinear, fwd+bwd, shared features"
+WORKLOADS = {
+    2: "cfg2: 2^20-point view-specific cloud, 1920x1080, C=4, bilinear 2x2 splats, fwd+bwd",
+    3: "cfg3: 4x2^20 ring-buffer cloud, 1920x1080, C=4, Gaussian splats (auto sigma, dilation 0.16), forward only",
+    4: "cfg4: 2^25-point global extracted cloud, 1920x1080, C=4, bilinear, forward only",
+    5: "cfg5: 64 orbit views of a 2^23-point static cloud, 1920x1080, C=4, bilinear, fwd+bwd, shared features",
+}
 NOMINAL_HBM_GBS = 8000.0
+DEFAULT_CONFIG = 5
 
 
 def peaks():
@@ -47,28 +57,40 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-# ------------------------------------------------------------------ byte model
-def algorithmic_bytes(N, Nv, Ft, P, C, sh=False, env=False, Fbig=0):
-    """Compulsory bytes per stage: each datum the method must
-    move, counted once, whatever the implementation re-reads.  (Sums over
-    views: N, Nv, Ft, P are totals.)  sh: features come as 9 SH coefficients
-    per channel (read 36 C B per visible point, gradient written 36 C B);
-    env: a C-channel background value per pixel, read in fwd and bwd.
-    Fbig: entries of tiles longer than the blend's in-warp sort (256), which
-    the big-tile sort reads once (8 B key) and writes once (4 B index)."""
+# ------------------------------------------------------------------ byte models
+def step_bytes_survey(N, Nv, Ft, P, C, fwd_only, sh=False, env=False):
+    """Compulsory bytes of one step, SURVEY.md §8(d) exactly (sums over the
+    views: N, Nv, Ft, P are totals):
+      B_fwd = 16 N + 4C Nv + 16 Ft + 4P(C+2) + 8P  [+ 4PC with a background]
+      B_bwd = 4P(C+2) + 8P + 4 Ft + (16+4C) Nv + 4(C+1) Nv
+    Variants (NEXT rows): SH features read 36C bytes per visible point and
+    write 36C bytes of coefficient gradients (f1); the env-map background
+    adds 4PC to both passes (f2)."""
+    fb = (36 if sh else 4) * C
+    b_fwd = 16 * N + fb * Nv + 16 * Ft + 4 * P * (C + 2) + 8 * P + (4 * P * C if env else 0)
+    b_bwd = 4 * P * (C + 2) + 8 * P + 4 * Ft + (16 + fb) * Nv + (fb + 4) * Nv + (4 * P * C if env else 0)
+    return b_fwd + (0 if fwd_only else b_bwd)
+
+
+def kernel_bytes(N, Nv, Ft, P, C, sh=False, env=False, F_mid=0, F_huge=0):
+    """Compulsory bytes per kernel, for the roofline of the
+    dominant kernel only -- NOT summed into the step (bin_fused is the sum of
+    project_count and scatter; the step model is step_bytes_survey).
+    F_mid / F_huge: entries of tiles of 257..2048 / over 2048 entries, which
+    the mid / big-tile sorts read once (8-byte key) and write once (4-byte
+    index)."""
     fbytes = (36 if sh else 4) * C
     m = {
-        "project_count": 12 * N + (fbytes * Nv if sh else 0),   # positions (+ SH coefficients)
+        "project_count": 12 * N + (fbytes * Nv if sh else 0),
         "scan_tiles": 0,
-        "scatter": 8 * Ft,                             # one write of the (key, idx) record
-        "sort_big": 12 * Fbig,
+        "scatter": 8 * Ft,
+        "sort_mid": 12 * F_mid,
+        "sort_big": 12 * F_huge,
         "blend_fwd": 8 * Ft + (4 + (0 if sh else 4 * C)) * Nv + 4 * P * (C + 2) + 8 * P,
-        #            record read, opacity+features, F/A/D write, T_final+last write
         "blend_bwd": 4 * P * (C + 2) + 8 * P + 4 * Ft + (16 + 4 * C) * Nv + 4 * (C + 1) * Nv,
-        #            upstream grads, saved state, sorted idx, xyz/o/f, gradient write
     }
     if sh:
-        m["sh_grad"] = 12 * Nv + fbytes * Nv           # positions (directions) + coefficient gradients
+        m["sh_grad"] = 12 * Nv + fbytes * Nv
     if env:
         m["blend_fwd"] += 4 * C * P
         m["blend_bwd"] += 4 * C * P
@@ -125,20 +147,28 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-# ------------------------------------------------------------------ CPU oracle leg
-def oracle_step(c, gF, gA, gD, frac, threads):
-    """Oracle fwd+bwd on a band of pixel rows covering `frac` of the frame."""
-    import oracle
-    H, W = c["H"], c["W"]
-    rows = max(1, int(round(frac * H)))
-    mask = np.zeros((H, W), np.uint8)
-    mask[:rows] = 1
-    t0 = time.perf_counter()
-    oracle.render(c["cams"][0], c["xyz"], c["feat"], c["opacity"], H, W, pixel_mask=mask,
-                  threads=threads)
-    oracle.backward(c["cams"][0], c["xyz"], c["feat"], c["opacity"], H, W, gF, gA, gD,
-                    pixel_mask=mask, threads=threads)
-    return time.perf_counter() - t0, rows / H
+# ------------------------------------------------------------------ workloads
+def load_workload(config, rank, world):
+    """Synthetic inputs of one config as seen by `rank`."""
+    from paper_2508_19140_b200.dist import assign_views
+    if config == 5:
+        c = synthgen.config5()
+        views = list(assign_views(64, world, rank))
+        return dict(c=c, cams=[c["cams"][v] for v in views], views=views, fwd_only=False,
+                    frames_per_step=64, scaling="strong", static=True, seed_g=5 + rank,
+                    parallelism=f"64 views split over {world} rank(s), one flat gradient all-reduce per step")
+    if config == 4:
+        c = synthgen.config4()
+        return dict(c=c, cams=c["cams"], views=[0], fwd_only=True, frames_per_step=1,
+                    scaling="strong" if world > 1 else "weak", static=True, seed_g=4,
+                    parallelism=(f"one frame in {world} screen bands + one all-gather" if world > 1 else "one frame"))
+    if config == 3:
+        c = synthgen.config3()
+        return dict(c=c, cams=c["cams"], views=[0], fwd_only=True, frames_per_step=world, scaling="weak",
+                    static=False, seed_g=3 + rank, parallelism=f"independent frames x{world}")
+    c = synthgen.config2(seed=2 + rank)
+    return dict(c=c, cams=c["cams"], views=[0], fwd_only=False, frames_per_step=world, scaling="weak",
+                static=False, seed_g=2 + rank, parallelism=f"independent frames x{world} (weak)")
 
 
 def cpu_threads():
@@ -148,37 +178,73 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+def oracle_view(c, v, gF, gA, gD, threads, fwd_only, pixel_mask=None):
+    """The CPU oracle on one whole view (fwd, + bwd unless fwd_only); seconds."""
+    import oracle
+    H, W = c["H"], c["W"]
+    cam = c["cams"][v]
+    kw = {} if c["mode"] == "bilinear" else dict(mode="gaussian", sigma=0.0, dilation=0.16)
+    t0 = time.perf_counter()
+    oracle.render(cam, c["xyz"], c["feat"], c["opacity"], H, W, pixel_mask=pixel_mask, threads=threads, **kw)
+    if not fwd_only:
+        oracle.backward(cam, c["xyz"], c["feat"], c["opacity"], H, W, gF, gA, gD, pixel_mask=pixel_mask,
+                        threads=threads, **kw)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(config, budget_s=12.0):
+    """Oracle throughput on whole views of the workload (frames/s)."""
+    w = load_workload(config, 0, 1)
+    c = w["c"]
+    H, W, C = c["H"], c["W"], c["C"]
+    gF, gA, gD = (x[0] for x in synthgen.upstream_grads(w["seed_g"], 1, H, W, C))
+    th = cpu_threads()
+    tt, nv, v = 0.0, 0, 0
+    while tt < budget_s or nv == 0:
+        tt += oracle_view(c, v % len(c["cams"]), gF, gA, gD, th, w["fwd_only"])
+        nv += 1
+        v += 21
+    return {"value": nv / tt, "unit": "frames/s", "cores": th, "kind": "oracle",
+            "sample": f"{nv} whole view(s) of {c['name']} ({'fwd' if w['fwd_only'] else 'fwd+bwd'}), "
+                      f"{tt:.1f} s on {th} threads"}
+
+
 def run_reference(args, rank, world):
+    """Reference arm: the CPU oracle as it stands, whole views per step (a
+    band of one view's rows only when (K + W) whole views would not fit the
+    few-minute budget)."""
     if rank != 0:
         return
-    c = synthgen.config2()
+    w = load_workload(args.config, 0, 1)
+    c = w["c"]
     H, W, C = c["H"], c["W"], c["C"]
-    gF, gA, gD = (x[0] for x in synthgen.upstream_grads(2, 1, H, W, C))
-    th = cpu_threads()
-    # size the per-step sample so the whole run stays within ~2 minutes
-    t_cal, f_cal = oracle_step(c, gF, gA, gD, 0.05, th)
-    per_frame = t_cal / f_cal
-    budget = 120.0 / max(1, args.steps + args.warmup)
-    frac = float(min(1.0, max(0.01, budget / per_frame)))
-    for _ in range(args.warmup):
-        oracle_step(c, gF, gA, gD, frac, th)
-    tt, ff = 0.0, 0.0
-    for _ in range(args.steps):
-        t, f = oracle_step(c, gF, gA, gD, frac, th)
-        tt += t
-        ff += f
-    fps = ff / tt
     N = c["xyz"].shape[0]
-    sample = f"{ff:.3f} frames ({args.steps} steps x {frac:.3f} of the 1080p rows) of cfg2 fwd+bwd"
+    gF, gA, gD = (x[0] for x in synthgen.upstream_grads(w["seed_g"], 1, H, W, C))
+    th = cpu_threads()
+    t_view = oracle_view(c, 0, gF, gA, gD, th, w["fwd_only"])
+    budget = 180.0 / max(1, args.steps + args.warmup)
+    frac = 1.0 if t_view <= budget else max(0.02, budget / t_view)
+    mask = None
+    if frac < 1.0:
+        mask = np.zeros((H, W), np.uint8)
+        mask[: max(1, int(round(frac * H)))] = 1
+        frac = float(mask[:, 0].mean())
+    tt = 0.0
+    for k in range(args.warmup + args.steps):
+        t = oracle_view(c, (21 * k) % len(c["cams"]), gF, gA, gD, th, w["fwd_only"], mask)
+        if k >= args.warmup:
+            tt += t
+    fps = args.steps * frac / tt
+    sample = (f"{args.steps} step(s) x " + ("one whole view" if frac == 1.0 else f"{frac:.3f} of a view's rows")
+              + f" of {c['name']} ({'fwd' if w['fwd_only'] else 'fwd+bwd'})")
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True, "scaling": w["scaling"],
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "N": N, "H": H, "W": W, "C": C},
+        "config": {"workload": WORKLOADS[args.config], "N": N, "H": H, "W": W, "C": C},
         "mpoints_per_s": fps * N / 1e6,
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": th, "kind": "oracle",
-                         "sample": sample},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": th, "kind": "oracle", "sample": sample},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -223,7 +289,7 @@ def run_sort_ab(args):
     fwd_us = st["blend_fwd"][0] / reps * 1e3
     pbits = (H * W - 1).bit_length()
     line = {
-        "mode": "sort A/B (NEXT f4)", "workload": WORKLOAD,
+        "mode": "sort A/B (NEXT f4)", "workload": WORKLOADS[2],
         "original_single_sort": {"us": single_us, "keys": 4 * N, "real_fragments": F,
                                  "key_bits": 32 + pbits, "passes": math.ceil((32 + pbits) / 8),
                                  "keys_per_s": 4 * N / (single_us * 1e-6),
@@ -243,29 +309,15 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_2508_19140_b200 as inpc
+    from paper_2508_19140_b200 import dist as pdist
 
     dev_index = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
-    if args.config == 5:
-        # training-style view batch (configs[4]): 64 orbit views of a 2^23
-        # cloud, shared features, views split over ranks, gradients all-reduced
-        c = synthgen.config5()
-        views = [v for v in range(64) if v * world // 64 == rank]   # contiguous blocks
-        cams = [c["cams"][v] for v in views]
-        seed_g = 5 + rank
-    elif args.config in (3, 4):
-        # forward-only inference frames: cfg3 ring-buffer cloud with Gaussians,
-        # cfg4 global extracted cloud (bilinear); one frame per rank
-        c = synthgen.config3() if args.config == 3 else synthgen.config4()
-        cams = c["cams"]
-        seed_g = args.config + rank
-    else:
-        c = synthgen.config2(seed=2 + rank)
-        cams = c["cams"]
-        seed_g = 2 + rank
+    wl = load_workload(args.config, rank, world)
+    c, cams = wl["c"], wl["cams"]
     mode = c["mode"]
-    fwd_only = args.config in (3, 4)
+    fwd_only = wl["fwd_only"]
     V = len(cams)
     H, W, C = c["H"], c["W"], c["C"]
     N = c["xyz"].shape[0]
@@ -274,94 +326,97 @@ def run_ours(args, rank, world, local_rank):
     feat_np = c["feat"]
     if args.variant in ("sh", "sh+env"):
         flags |= inpc.FLAG_SH_FEATURES
-        feat_np = np.random.default_rng(seed_g + 11).normal(0, 0.5, (N, C, 9)).astype(np.float32)
-    env_hw = None
-    env_t = None
+        feat_np = np.random.default_rng(wl["seed_g"] + 11).normal(0, 0.5, (N, C, 9)).astype(np.float32)
+    env_hw = env_t = None
     if args.variant in ("env", "sh+env"):
         env_hw = (1024, 2048)   # the paper's distilled map size
-        env_t = torch.from_numpy(np.random.default_rng(seed_g + 12).uniform(
+        env_t = torch.from_numpy(np.random.default_rng(wl["seed_g"] + 12).uniform(
             -1, 1, (1024, 2048, C)).astype(np.float32)).to(dev)
-    xyz_h = torch.from_numpy(c["xyz"]).pin_memory()
-    feat_h = torch.from_numpy(feat_np).pin_memory()
-    op_h = torch.from_numpy(c["opacity"]).pin_memory()
-    xyz, feat, op = xyz_h.to(dev), feat_h.to(dev), op_h.to(dev)
-    if world > 1 and args.config in (4, 5):
-        # one cloud for all ranks: broadcast once from rank 0 (untimed; NCCL over NVLink)
-        from paper_2508_19140_b200 import dist as pdist
-        pdist.broadcast_cloud([xyz, feat, op])
-    bands = None
+    ctx = inpc.Context(dev_index)
+    xyz = torch.from_numpy(c["xyz"]).to(dev)
+    feat = torch.from_numpy(feat_np).to(dev)
+    op = torch.from_numpy(c["opacity"]).to(dev)
+    order = args.order if args.order != "auto" else ("spatial" if wl["static"] else "given")
+    prepare_ms = None
+    if order == "spatial":
+        # one-time spatial order of the static cloud (untimed, reported)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx.spatial_order(xyz)          # warm (buffer allocation)
+        e0.record()
+        perm = ctx.spatial_order(xyz)
+        xyz, feat, op = xyz[perm].contiguous(), feat[perm].contiguous(), op[perm].contiguous()
+        e1.record()
+        torch.cuda.synchronize()
+        prepare_ms = e0.elapsed_time(e1)
+        del perm
+    if world > 1 and wl["static"]:
+        pdist.broadcast_cloud([xyz, feat, op])    # one cloud for all ranks, once (NCCL over NVLink)
+    # host copies (pinned) in the order the device uses, for the end-to-end leg
+    xyz_h, feat_h, op_h = (t.cpu().pin_memory() for t in (xyz, feat, op))
+    bands = asm = None
     if args.config == 4 and world > 1:
         # sort-first screen bands of 8-pixel tile rows, balanced by the per-row
         # tile-entry counts of the (static) cloud, measured once untimed
-        from paper_2508_19140_b200 import dist as pdist
-        probe = inpc.Context(dev_index)
-        probe.forward(inpc.make_cfg(H, W, C, c["mode"]), cams, xyz, feat, op)
-        rng = probe.debug_export(0, H=H, W=W)["tile_ranges"].cpu().numpy().astype(np.int64)
-        probe.close()
+        ctx.forward(inpc.make_cfg(H, W, C, mode), cams, xyz, feat, op)
+        rng = ctx.debug_export(0, H=H, W=W)["tile_ranges"].cpu().numpy().astype(np.int64)
         tx = (W + 7) // 8
-        per_tile = np.diff(rng)
-        row_w = per_tile.reshape(-1, tx).sum(1) + 64 * tx   # + per-pixel output cost
+        row_w = np.diff(rng).reshape(-1, tx).sum(1) + 64 * tx   # + per-pixel output cost
         bands = pdist.band_split(row_w, world)
-    if args.config == 5:
-        # one (V, H, W) block of upstream gradients shared by the rank's views
-        g1 = [torch.from_numpy(x) for x in synthgen.upstream_grads(seed_g, 1, H, W, C)]
-        gF_h, gA_h, gD_h = (x.expand((V,) + tuple(x.shape[1:])).contiguous().pin_memory() for x in g1)
-    else:
-        gF_h, gA_h, gD_h = (torch.from_numpy(x).pin_memory() for x in synthgen.upstream_grads(seed_g, 1, H, W, C))
+        asm = pdist.BandAssembler(H, bands, (W, C + 2), device=dev)
+    g1 = [torch.from_numpy(x) for x in synthgen.upstream_grads(wl["seed_g"], 1, H, W, C)]
+    gF_h, gA_h, gD_h = (x.expand((V,) + tuple(x.shape[1:])).contiguous().pin_memory() for x in g1)
     gF, gA, gD = gF_h.to(dev), gA_h.to(dev), gD_h.to(dev)
-    ctx = inpc.Context(dev_index)
     cfg = inpc.make_cfg(H, W, C, mode, flags=flags, env_hw=env_hw,
                         band=None if bands is None else bands[rank])
     out = dict(F=torch.empty((V, H, W, C), device=dev), A=torch.empty((V, H, W), device=dev),
                D=torch.empty((V, H, W), device=dev))
-    g_feat = torch.zeros_like(feat)
-    g_op = torch.zeros_like(op)
+    if args.variant in ("sh", "sh+env"):
+        g_flat = None
+        g_feat = torch.zeros_like(feat)
+        g_op = torch.zeros_like(op)
+    else:
+        g_flat, g_feat, g_op = pdist.flat_grad_buffers(N, C, device=dev)
     reduce_grads = args.config == 5 and world > 1
+    img_cat = torch.empty((H, W, C + 2), device=dev) if asm is not None else None
 
-    slab = gathered = None
-    if bands is not None:
-        max_rows = max((e - b) * 8 for b, e in bands)
-        slab = torch.zeros((max_rows, W, C + 2), device=dev)
-        gathered = [torch.empty_like(slab) for _ in range(world)]
-        full = torch.empty((H, W, C + 2), device=dev)
-
-    def step():
+    def step(S=None):
+        S = S or dict(xyz=xyz, feat=feat, op=op, gF=gF, gA=gA, gD=gD, out=out, g_flat=g_flat,
+                      g_feat=g_feat, g_op=g_op)
         if fwd_only:
-            ctx.forward(cfg, cams, xyz, feat, op, bg=env_t, out=out)
-            if bands is not None:   # assemble the frame: all-gather of the bands
-                b0, b1 = bands[rank]
-                r0, r1 = b0 * 8, min(b1 * 8, H)
-                slab[: r1 - r0, :, :C] = out["F"][0, r0:r1]
-                slab[: r1 - r0, :, C] = out["A"][0, r0:r1]
-                slab[: r1 - r0, :, C + 1] = out["D"][0, r0:r1]
-                dist.all_gather(gathered, slab)
-                for r, (q0, q1) in enumerate(bands):
-                    a0, a1 = q0 * 8, min(q1 * 8, H)
-                    full[a0:a1] = gathered[r][: a1 - a0]
+            ctx.forward(cfg, cams, S["xyz"], S["feat"], S["op"], bg=env_t, out=S["out"])
+            if asm is not None:   # assemble the frame: one all-gather of the padded bands
+                rs = asm.band_rows(rank)
+                img_cat[rs, :, :C] = S["out"]["F"][0, rs]
+                img_cat[rs, :, C] = S["out"]["A"][0, rs]
+                img_cat[rs, :, C + 1] = S["out"]["D"][0, rs]
+                asm.pack(rank, img_cat)
+                asm.gather()
             return
-        g_feat.zero_()
-        g_op.zero_()
-        ctx.forward(cfg, cams, xyz, feat, op, bg=env_t, out=out)
-        ctx.backward(cfg, cams, xyz, feat, op, gF, gA, gD, bg=env_t, g_feat=g_feat, g_opacity=g_op)
+        if S["g_flat"] is not None:
+            S["g_flat"].zero_()
+        else:
+            S["g_feat"].zero_()
+            S["g_op"].zero_()
+        ctx.forward(cfg, cams, S["xyz"], S["feat"], S["op"], bg=env_t, out=S["out"])
+        ctx.backward(cfg, cams, S["xyz"], S["feat"], S["op"], S["gF"], S["gA"], S["gD"], bg=env_t,
+                     g_feat=S["g_feat"], g_opacity=S["g_op"])
         if reduce_grads:   # the view batch's one exchange step (shared features, R20)
-            dist.all_reduce(g_feat)
-            dist.all_reduce(g_op)
+            dist.all_reduce(S["g_flat"])
 
     # workload statistics (untimed): visible points, tile entries, per view
     dbg = inpc.make_cfg(H, W, C, mode, flags=flags | inpc.FLAG_DEBUG, env_hw=env_hw)
     ctx.forward(dbg, cams, xyz, feat, op, bg=env_t)
-    Nv = Ft = Fbig = 0
+    Nv = Ft = F_mid = F_huge = 0
     for v in range(V):
         ex = ctx.debug_export(v, N=N, H=H, W=W)
         Nv += int((ex["tiles_touched"] > 0).sum().item())
         Ft += int(ex["F_t"])
         cnt = ex["tile_ranges"][1:].long() - ex["tile_ranges"][:-1].long()
-        Fbig += int(cnt[cnt > 256].sum().item())
-    model = algorithmic_bytes(N * V, Nv, Ft, P * V, C, sh="sh" in args.variant,
-                              env="env" in args.variant, Fbig=Fbig)
-    if fwd_only:
-        model = {k: v for k, v in model.items() if k not in ("blend_bwd", "sh_grad")}
-    step_bytes = sum(model.values())
+        F_mid += int(cnt[(cnt > 256) & (cnt <= 2048)].sum().item())
+        F_huge += int(cnt[cnt > 2048].sum().item())
+    sh, env = "sh" in args.variant, "env" in args.variant
+    kmodel = kernel_bytes(N * V, Nv, Ft, P * V, C, sh=sh, env=env, F_mid=F_mid, F_huge=F_huge)
+    step_bytes = step_bytes_survey(N * V, Nv, Ft, P * V, C, fwd_only, sh=sh, env=env)
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     for _ in range(args.warmup):
@@ -373,8 +428,9 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
     graph = None
     graph_launches = 0
-    if not args.no_graph:
-        # one step captured as a CUDA graph: our 6 kernels + the two gradient memsets
+    if not args.no_graph and world == 1:
+        # one step captured as a CUDA graph (our kernels + the gradient memset);
+        # at N > 1 the step keeps its NCCL collective and runs eagerly
         try:
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
@@ -386,17 +442,15 @@ def run_ours(args, rank, world, local_rank):
             ctx.stage_times(reset=True)
             with torch.cuda.graph(graph):
                 step()
-            # kernels per replay (counted by the library at capture)
             graph_launches = int(sum(v[1] for v in ctx.stage_times(reset=True).values()))
             graph.replay()
             torch.cuda.synchronize()
         except Exception as e:  # pragma: no cover - reported in the JSON line
             print(f"graph capture failed, eager timing: {e}", file=sys.stderr)
             graph = None
-    # per-stage device time (CUDA events around each stage on the launching
-    # stream): live in the timed region when eager; with a graph, events
-    # inside the graph cannot be timed, so each timed replay is followed by
-    # one eager profiled step (outside the per-step events).
+    # per-stage device time: CUDA events around each stage on the launching
+    # stream; with a graph (events inside a graph cannot be timed) each timed
+    # replay is followed by one eager profiled step outside the step events
     ctx.stage_times(reset=True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -404,7 +458,7 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     ctx.set_profiling(graph is None)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         for k in range(args.steps):
             flush.fill_(float(k))          # evict L2 between steps (outside the step events)
             ev[k][0].record()
@@ -432,8 +486,7 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     ms_per_step = tot_ms / args.steps
-    frames_per_step = 64 if args.config == 5 else (1 if bands is not None else world)
-    fps = frames_per_step * args.steps / (tot_ms / 1e3)
+    fps = wl["frames_per_step"] * args.steps / (tot_ms / 1e3)
     # our kernels launched inside the timed region: the profiled eager steps
     # (counted by the library) plus, with a graph, the kernels of each replay
     launches = int(sum(v[1] for v in stages.values())) + (graph_launches * args.steps if graph_used else 0)
@@ -442,13 +495,15 @@ def run_ours(args, rank, world, local_rank):
     hbm, peak_src = peaks()
     kern = {k: v for k, v in stages.items() if v[1] > 0}
     dom = max(kern, key=lambda k: kern[k][0])
+    launches_per_step = max(1, round(kern[dom][1] / args.steps))
     dom_ms = kern[dom][0] / kern[dom][1]
-    dom_bytes = model.get(dom, 0) / max(1, round(kern[dom][1] / args.steps))   # per launch (per view)
+    dom_bytes = kmodel.get(dom, 0) / launches_per_step                # per launch (per view)
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
-            "bytes_per_launch": dom_bytes, "us_per_launch": dom_ms * 1e3}
-    prof_traffic = os.path.join(ROOT, "profiles", "traffic_r01.json")
+            "bytes_per_launch": dom_bytes, "us_per_launch": dom_ms * 1e3,
+            "share_of_step": kern[dom][0] / args.steps / ms_per_step}
+    prof_traffic = os.path.join(ROOT, "profiles", "traffic_r02.json")
     if os.path.exists(prof_traffic):
         trj = json.load(open(prof_traffic))
         key = f"cfg{args.config}" + ("" if args.variant == "base" else "-" + args.variant)
@@ -457,25 +512,30 @@ def run_ours(args, rank, world, local_rank):
             roof["traffic"] = tr
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
 
-    # end to end through the public API with host (pinned) buffers
+    # end to end through the public API with host (pinned) buffers: every step
+    # copies its inputs in (cloud + upstream gradients) and its results out
+    # (image + gradients); two device buffer sets so that step k+1's H2D and
+    # step k-1's D2H overlap step k
     F_h = torch.empty((V, H, W, C), pin_memory=True)
     A_h = torch.empty((V, H, W), pin_memory=True)
     D_h = torch.empty((V, H, W), pin_memory=True)
-    gf_h = torch.empty_like(feat_h).pin_memory()
-    go_h = torch.empty_like(op_h).pin_memory()
-    h2d = sum(t.numel() * 4 for t in (xyz_h, feat_h, op_h, gF_h, gA_h, gD_h))
-    d2h = sum(t.numel() * 4 for t in (F_h, A_h, D_h, gf_h, go_h))
-
-    if fwd_only:
-        h2d = sum(t.numel() * 4 for t in (xyz_h, feat_h, op_h))
-        d2h = sum(t.numel() * 4 for t in (F_h, A_h, D_h))
-
-    # two device buffer sets so that step k+1's H2D and step k-1's D2H overlap
-    # step k's kernels (three streams; a serving / training input pipeline)
-    sets = [dict(xyz=xyz, feat=feat, op=op, gF=gF, gA=gA, gD=gD, out=out, g_feat=g_feat, g_op=g_op)]
+    gf_h = torch.empty(tuple(feat.shape), pin_memory=True)
+    go_h = torch.empty(tuple(op.shape), pin_memory=True)
+    ins = (xyz_h, feat_h, op_h) + (() if fwd_only else (gF_h, gA_h, gD_h))
+    outs = (F_h, A_h, D_h) + (() if fwd_only else (gf_h, go_h))
+    h2d = sum(t.numel() * 4 for t in ins)
+    d2h = sum(t.numel() * 4 for t in outs)
+    sets = [dict(xyz=xyz, feat=feat, op=op, gF=gF, gA=gA, gD=gD, out=out, g_flat=g_flat, g_feat=g_feat,
+                 g_op=g_op)]
     if not args.profile_run:
-        sets.append({k: (v.clone() if torch.is_tensor(v) else {kk: vv.clone() for kk, vv in v.items()})
-                     for k, v in sets[0].items()})
+        S2 = {k: (v.clone() if torch.is_tensor(v) else ({kk: vv.clone() for kk, vv in v.items()}
+                                                        if isinstance(v, dict) else v))
+              for k, v in sets[0].items() if k not in ("g_flat", "g_feat", "g_op")}
+        if g_flat is not None:
+            S2["g_flat"], S2["g_feat"], S2["g_op"] = pdist.flat_grad_buffers(N, C, device=dev)
+        else:
+            S2["g_flat"], S2["g_feat"], S2["g_op"] = None, torch.zeros_like(feat), torch.zeros_like(op)
+        sets.append(S2)
     s_comp = torch.cuda.current_stream()
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in sets]
@@ -499,17 +559,7 @@ def run_ours(args, rank, world, local_rank):
             ev_in[b].record(s_h2d)
         s_comp.wait_event(ev_in[b])
         s_comp.wait_event(ev_read[b])             # set b's previous outputs were copied out
-        if fwd_only:
-            ctx.forward(cfg, cams, S["xyz"], S["feat"], S["op"], bg=env_t, out=S["out"])
-        else:
-            S["g_feat"].zero_()
-            S["g_op"].zero_()
-            ctx.forward(cfg, cams, S["xyz"], S["feat"], S["op"], bg=env_t, out=S["out"])
-            ctx.backward(cfg, cams, S["xyz"], S["feat"], S["op"], S["gF"], S["gA"], S["gD"], bg=env_t,
-                         g_feat=S["g_feat"], g_opacity=S["g_op"])
-            if reduce_grads:
-                dist.all_reduce(S["g_feat"])
-                dist.all_reduce(S["g_op"])
+        step(S)
         ev_done[b].record(s_comp)
         with torch.cuda.stream(s_d2h):
             s_d2h.wait_event(ev_done[b])
@@ -523,8 +573,10 @@ def run_ours(args, rank, world, local_rank):
 
     for k in range(0 if args.profile_run else 2):
         e2e_step(k)
-    n_e2e = 1 if args.profile_run else max(4, min(args.steps, 20))
+    n_e2e = 1 if args.profile_run else max(4, min(args.steps, 10))
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s_h2d)
     for k in range(n_e2e):
@@ -537,48 +589,36 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_fps = frames_per_step / (e2e_ms / 1e3)
+    e2e_fps = wl["frames_per_step"] / (e2e_ms / 1e3)
 
-    # CPU oracle baseline (rank 0, N = 1 only): bounded sample of the same workload
+    # CPU oracle baseline (rank 0, N = 1 only): whole views of the same workload
     cpu = None
-    if (rank == 0 and world == 1 and args.config == 2 and args.variant == "base"
-            and not (args.no_cpu_baseline or args.profile_run)):
-        th = cpu_threads()
-        gFn, gAn, gDn = (x[0] for x in synthgen.upstream_grads(2, 1, H, W, C))
-        tt, ff = 0.0, 0.0
-        while tt < 10.0:
-            t, f = oracle_step(c, gFn, gAn, gDn, 0.25, th)
-            tt += t
-            ff += f
-        cpu = {"value": ff / tt, "unit": "frames/s", "cores": th, "kind": "oracle",
-               "sample": f"{ff:.2f} frames (bands of 25 % of the 1080p rows) of cfg2 fwd+bwd, {tt:.1f} s"}
+    if rank == 0 and world == 1 and args.variant == "base" and not (args.no_cpu_baseline or args.profile_run):
+        cpu = cpu_baseline(args.config)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "passes": "fwd" if fwd_only else "fwd+bwd",
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True,
-            "scaling": "strong" if (args.config == 5 or bands is not None) else "weak",
+            "higher_is_better": True, "scaling": wl["scaling"],
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": {5: WORKLOAD5, 3: WORKLOAD3, 4: WORKLOAD4}.get(args.config, WORKLOAD),
-                       "variant": args.variant, "N": N, "views_per_rank": V,
-                       "N_visible": Nv, "F_t": Ft, "F_big": Fbig, "H": H, "W": W,
+            "config": {"workload": WORKLOADS[args.config], "variant": args.variant, "N": N,
+                       "views_per_step": wl["frames_per_step"], "views_per_rank": V,
+                       "N_visible": Nv, "F_t": Ft, "F_mid": F_mid, "F_huge": F_huge, "H": H, "W": W,
                        "C": C, "mode": mode, "alpha_max": 0.99, "t_min": 1e-4,
-                       "parallelism": (f"64 views split over {world} ranks + gradient all-reduce"
-                                       if args.config == 5 else
-                                       (f"one frame in {world} screen bands {bands} + all-gather"
-                                        if bands is not None else f"independent frames x{world} (weak)")),
+                       "point_order": order, "parallelism": wl["parallelism"],
                        "l2": "flushed: 256 MiB write between steps, outside the per-step events"},
             "mpoints_per_s": fps * N / 1e6,
+            "prepare_ms": prepare_ms,
             "step_algorithmic_bytes": step_bytes,
+            "step_bytes_model": "SURVEY.md §8(d) B_fwd" + ("" if fwd_only else " + B_bwd"),
             "step_roofline": {"achieved": step_gbs, "peak": hbm, "unit": "GB/s", "frac": step_gbs / hbm,
                               "frac_of_nominal_8TBs": step_gbs / NOMINAL_HBM_GBS},
             "roofline": roof,
             "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items() if v[1]},
             "stages_note": ("device time per stage from CUDA events around each stage of an eager "
-                            "profiled step after every timed replay (same kernels as the graph); "
-                            "bin_fused = project + scan + scatter + big-tile sort in one cooperative launch"),
+                            "profiled step after every timed replay (same kernels as the graph)"),
             "gpu_launches": launches,
             "cuda_graph": graph_used,
             "clocks": clk.summary(),
@@ -593,20 +633,38 @@ def run_ours(args, rank, world, local_rank):
     ctx.close()
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_cmd(gpus, argv, port):
+    """torchrun command that re-runs this script with `gpus` ranks."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
-    ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2,
-                    help="2: cfg2 frame per rank (default, weak scaling); 3/4: forward-only "
-                         "inference frames (Gaussian ring buffer / 33M global cloud); 5: 64-view "
-                         "batch split over ranks with a gradient all-reduce (strong scaling)")
+    ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=DEFAULT_CONFIG,
+                    help="5 (default, north star): 64-view batch of a static 2^23 cloud split over ranks "
+                         "+ one gradient all-reduce (strong scaling); 2: cfg2 frame per rank (weak); "
+                         "3/4: forward-only inference frames (Gaussian ring buffer / 33M global cloud, "
+                         "screen bands at N > 1)")
     ap.add_argument("--variant", choices=["base", "sh", "env", "sh+env"], default="base",
                     help="NEXT rows: SH-coefficient features (f1) / env-map background (f2)")
+    ap.add_argument("--order", choices=["auto", "given", "spatial"], default="auto",
+                    help="point order: auto = spatial (one-time Morton order) for the static clouds "
+                         "of cfg4/cfg5, as generated for the per-frame clouds of cfg2/cfg3")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (GPUs) or gloo (1-GPU tests)")
     ap.add_argument("--sort-ab", action="store_true",
                     help="NEXT f4: original single 64-bit sort vs the tiled ordering (one JSON line)")
@@ -614,9 +672,15 @@ def main():
                     help="for ncu: no clock ramp, no e2e leg, no CPU baseline")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # self-launch: one process per GPU under torch.distributed.run
+        cmd = relaunch_cmd(args.gpus, sys.argv[1:], _free_port())
+        os.execv(cmd[0], cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"note: WORLD_SIZE={world} ranks, --gpus {args.gpus}", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

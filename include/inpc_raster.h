@@ -190,6 +190,19 @@ INPC_API int inpc_sort_single64(inpc_ctx* ctx, const inpc_raster_cfg* cfg, const
                                 const float* xyz, const float* opacity, int64_t N, uint32_t* pixel_ranges,
                                 uint32_t* sorted_idx, int64_t sorted_cap, int64_t* F_out, void* stream);
 
+/* One-time spatial ordering of a static cloud (not a step of the method;
+ * DESIGN.md §6): perm [N] u32 (device) receives the permutation that sorts
+ * the points by the 30-bit Morton code of their position on a 1024^3 grid
+ * over the cloud's bounding box (stable; non-finite points last).  A caller
+ * with a static cloud (the pre-extracted global cloud;
+ * the shared cloud of a view batch) gathers xyz / features / opacities by
+ * perm once and rasterizes the reordered cloud: point indices (and the
+ * tie-break of equal depths, R8) then refer to the reordered cloud.  Spatial
+ * order makes the tile-slot atomics, tile buckets, record gathers and
+ * gradient atomics local (warp-aggregated, L2-resident).  xyz [N,3] device.
+ * Asynchronous on stream. */
+INPC_API int inpc_spatial_order(inpc_ctx* ctx, const float* xyz, int64_t N, uint32_t* perm, void* stream);
+
 /* Per-stage device timing (CUDA events around each stage; adds no sync to
  * the calls).  inpc_ctx_stage_times waits for the recorded events, adds
  * their elapsed milliseconds to per-stage accumulators and returns the

@@ -33,7 +33,7 @@ TILE = 8
 EXPORTS = ("inpc_ctx_create", "inpc_ctx_destroy", "inpc_rasterize_fwd", "inpc_rasterize_bwd",
            "inpc_debug_export", "inpc_ctx_set_profiling", "inpc_ctx_stage_times",
            "inpc_ctx_forget_events", "inpc_ctx_set_allocator", "inpc_sort_single64",
-           "inpc_stage_name", "inpc_status_string", "inpc_version")
+           "inpc_stage_name", "inpc_status_string", "inpc_version", "inpc_spatial_order")
 
 
 # inpc_alloc_fn / inpc_free_fn (include/inpc_raster.h)
@@ -72,6 +72,15 @@ def _load():
             raise ImportError(f"{LIB_PATH} is missing and could not be built ({e}); build it with "
                               "`python -m paper_2508_19140_b200.build` (nvcc, sm_100a); "
                               "there is no CPU fallback") from e
+    else:
+        from . import build as _build
+        if _build.stale():
+            # not rebuilt on import (minutes of nvcc; a copied tree may carry
+            # newer source mtimes): say so, the struct layouts may differ
+            import warnings
+            warnings.warn(f"{LIB_PATH} is older than its sources or was built with other flags "
+                          f"({_build.built_flags()!r}); rebuild with `python -m paper_2508_19140_b200.build`",
+                          RuntimeWarning, stacklevel=2)
     lib = ct.CDLL(LIB_PATH)
     P, i32, i64 = ct.c_void_p, ct.c_int32, ct.c_int64
     lib.inpc_ctx_create.argtypes = [ct.POINTER(P), ct.c_int]
@@ -85,6 +94,7 @@ def _load():
     lib.inpc_ctx_forget_events.argtypes = [P]
     lib.inpc_sort_single64.argtypes = [P, P, P, P, P, i64, P, P, i64, ct.POINTER(i64), P]
     lib.inpc_ctx_set_allocator.argtypes = [P, ALLOC_FN, FREE_FN, P]
+    lib.inpc_spatial_order.argtypes = [P, P, i64, P, P]
     lib.inpc_stage_name.argtypes = [i32]
     lib.inpc_stage_name.restype = ct.c_char_p
     lib.inpc_status_string.argtypes = [ct.c_int]
@@ -292,6 +302,16 @@ class Context:
         _check(lib.inpc_sort_single64(self._h, ct.byref(cfg), cam_arr, _ptr(xyz), _ptr(opacity), N,
                                       _ptr(ranges), _ptr(idx), idx.numel(), ct.byref(F), _stream(stream)))
         return ranges, idx[:F.value]
+
+    def spatial_order(self, xyz, stream=None):
+        """Permutation (int64 CUDA tensor [N]) that puts a static cloud in
+        Morton order (inpc_spatial_order); gather every per-point array by it
+        once, then rasterize the reordered cloud."""
+        import torch
+        N = xyz.shape[0]
+        perm = torch.empty(max(N, 1), dtype=torch.int32, device=xyz.device)
+        _check(lib.inpc_spatial_order(self._h, _ptr(xyz), N, _ptr(perm), _stream(stream)))
+        return perm[:N].long()
 
     def set_profiling(self, on=True):
         _check(lib.inpc_ctx_set_profiling(self._h, 1 if on else 0))

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libinpc_raster.so")
 SOURCES = [os.path.join(CSRC, "inpc_raster.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "raster_math.cuh", "single_sort.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "raster_math.cuh", "single_sort.cuh", "spatial_order.cuh")] + [
     os.path.join(ROOT, "include", "inpc_raster.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -24,18 +24,41 @@ FLAGS = [
 ]
 
 
+FLAGS_FILE = LIB + ".flags"
+
+
+def _extra():
+    # diagnostics only, e.g. -DINPC_PHASE_TIMES
+    return os.environ.get("INPC_NVCC_EXTRA", "").split()
+
+
+def _flag_line(extra) -> str:
+    return " ".join(FLAGS + list(extra))
+
+
 def stale() -> bool:
+    """Library missing, older than a source, or built with other flags."""
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(d) > t for d in DEPS)
+    if any(os.path.getmtime(d) > t for d in DEPS):
+        return True
+    return built_flags() != _flag_line(_extra())
+
+
+def built_flags():
+    try:
+        with open(FLAGS_FILE) as f:
+            return f.read().strip()
+    except OSError:
+        return None
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    extra = os.environ.get("INPC_NVCC_EXTRA", "").split()   # diagnostics only, e.g. -DINPC_PHASE_TIMES
+    extra = _extra()
     cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC, *SOURCES, "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -46,6 +69,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
         f.write(r.stderr)
     os.replace(tmp, LIB)
+    with open(FLAGS_FILE, "w") as f:
+        f.write(_flag_line(extra) + "\n")
     return LIB
 
 

@@ -14,6 +14,7 @@
 #include "inpc_raster.h"
 #include "kernels.cuh"
 #include "single_sort.cuh"
+#include "spatial_order.cuh"
 
 using namespace inpc;
 
@@ -48,11 +49,12 @@ enum Stage : int {
   kStBin,
   kStShGrad,
   kStSingleSort,
+  kStSortMid,
   kNumStages
 };
 const char* kStageNames[kNumStages] = {"memset",    "project_count", "scan_tiles", "scatter",
                                        "sort_big",  "blend_fwd",     "blend_bwd",  "bin_fused",
-                                       "sh_grad",   "single_sort"};
+                                       "sh_grad",   "single_sort",   "sort_mid"};
 
 struct ViewState {
   Buf ranges, sorted_idx, T_final, last, dbg_key, dbg_tiles, scalars, rec, feat_eval;
@@ -70,9 +72,13 @@ struct inpc_ctx {
   int device = 0;
   int num_sms = 148;
   int big_grid = 0;
+  int mid_grid = 0;        // k_sort_mid: resident CTAs (grid-stride over the big-tile list)
+  bool no_mid_sort = false;
+  int mid_qbits = 16;       // depth bits of the warp mid sort's keys (2 passes of 8-bit digits)
+  uint32_t mid_warp_max = 0; // k_sort_mid: tiles up to this size are sorted by one warp, larger by the CTA // env INPC_NO_MID_SORT=1: every big tile through k_sort_big (A/B)
   // scratch (shared by views, stream ordered)
   Buf scat;  // unfused bilinear binning: depth key + tile block | corner mask per point
-  Buf zeroed, cursor, big_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg, g_eval;
+  Buf zeroed, cursor, big_tiles, huge_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg, g_eval;
   Buf f4_rec, f4_keys, f4_vals, f4_keys2, f4_vals2, f4_hist, f4_scan, f4_misc;  // NEXT f4 baseline
   int bin_grid[3] = {0, 0, 0};  // cooperative grid of k_bin_bilinear<2,4,8>
   bool no_fused_bin = false;     // env INPC_NO_FUSED_BIN=1: separate binning kernels
@@ -169,7 +175,7 @@ struct AllocScope {
 };
 
 void release_all(inpc_ctx* c) {
-  for (Buf* b : {&c->scat, &c->zeroed, &c->cursor, &c->big_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots,
+  for (Buf* b : {&c->scat, &c->zeroed, &c->cursor, &c->big_tiles, &c->huge_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots,
                  &c->agg, &c->g_eval, &c->tmp, &c->overflow, &c->f4_rec, &c->f4_keys, &c->f4_vals,
                  &c->f4_keys2, &c->f4_vals2, &c->f4_hist, &c->f4_scan, &c->f4_misc})
     free_buf(*b);
@@ -443,6 +449,20 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
   cudaFuncSetAttribute(k_sort_big, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_big, kBigThreadsLarge, big_smem);
   c->big_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
+  per_sm = 0;
+  cudaFuncSetAttribute(k_sort_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortMidSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_mid, kMidThreads, kSortMidSmem);
+  c->mid_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
+  {
+    const char* e = getenv("INPC_NO_MID_SORT");
+    c->no_mid_sort = e && e[0] == '1';
+    const char* w = getenv("INPC_MID_WARP_MAX");  // A/B: tiles up to this size sorted by one warp
+    c->mid_warp_max = w ? (uint32_t)atoi(w) : (uint32_t)kWarpMidMax;
+    if (c->mid_warp_max > (uint32_t)kWarpMidMax) c->mid_warp_max = kWarpMidMax;
+    const char* q = getenv("INPC_MID_QBITS");  // A/B: depth bits kept in the warp sort's 32-bit keys
+    c->mid_qbits = q ? atoi(q) : 16;
+    if (c->mid_qbits < 8 || c->mid_qbits > 22) c->mid_qbits = 16;
+  }
   {
     int o2 = 0, o4 = 0, o8 = 0;
     cudaFuncSetAttribute(k_bin_bilinear<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bin_smem_bytes<2>());
@@ -606,9 +626,11 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   if ((st = ensure(c->cursor, (size_t)(T + 1) * 4, s))) return st;
   if (!gauss && (st = ensure(c->slots, (size_t)(N > 0 ? N : 1) * 16, s))) return st;
   if ((st = ensure(c->big_tiles, (size_t)(T + 1) * 4, s))) return st;
+  if ((st = ensure(c->huge_tiles, (size_t)(T + 1) * 4, s))) return st;
   if ((st = ensure(c->big_elem, (size_t)(T + 2) * 4, s))) return st;
   if ((st = ensure(c->big_chunk, (size_t)(T + 2) * 4, s))) return st;
-  if ((st = ensure(c->overflow, 64, s))) return st;
+  if ((st = ensure(c->overflow, 64, s, &fresh))) return st;  // [0] Gaussian overflow flag, [4..5] k_sort_mid dispenser
+  if (fresh) CK(cudaMemsetAsync(c->overflow.p, 0, c->overflow.bytes, s));
   uint64_t bound = gauss ? 0 : 4ull * (uint64_t)N;  // bilinear: <= 4 tiles per point
   if (!gauss && bound >= 0xFFFFFFFFull) return INPC_KEY_OVERFLOW;
   if ((int)c->views.size() < V) c->views.resize(V);
@@ -730,7 +752,8 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       k_scan_tiles<<<scan_blocks, kScanThreads, 0, s>>>(T, tc, (uint32_t*)vs.ranges.p,
                                                         (uint32_t*)c->cursor.p,
                                                         (uint32_t*)c->big_tiles.p, scan_state, scan_ctl,
-                                                        sc);
+                                                        sc, c->no_mid_sort ? nullptr : (uint32_t*)c->huge_tiles.p,
+                                                        (uint32_t)kMidMax);
       CK(cudaGetLastError());
     }
     uint64_t need = bound;
@@ -760,8 +783,17 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
                                                        (unsigned long long*)c->entries.p, scp);
       CK(cudaGetLastError());
     }
+    if (N > kWarpSortCap && !fused_kp && !c->no_mid_sort) {  // tiles of 257..kMidMax entries
+      StageTimer tm(c, s, kStSortMid, 1);
+      k_sort_mid<<<c->mid_grid, kMidThreads, kSortMidSmem, s>>>((const uint32_t*)vs.ranges.p, (const uint32_t*)c->big_tiles.p,
+                                                     sc, (const unsigned long long*)c->entries.p,
+                                                     (uint32_t*)vs.sorted_idx.p, c->mid_warp_max, c->mid_qbits,
+                                                     (uint32_t*)c->overflow.p + 4);
+      CK(cudaGetLastError());
+    }
     if (N > kWarpSortCap && !fused_kp) {  // a tile can only exceed the cap with > cap points
       StageTimer tm(c, s, kStSortBig, 1);
+      uint32_t min_n = c->no_mid_sort ? (uint32_t)kWarpSortCap : (uint32_t)kMidMax;
       const uint32_t* r = (const uint32_t*)vs.ranges.p;
       const uint32_t* bt = (const uint32_t*)c->big_tiles.p;
       uint32_t* be = (uint32_t*)c->big_elem.p;
@@ -770,7 +802,9 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       unsigned long long* en = (unsigned long long*)c->entries.p;
       unsigned long long* tp = (unsigned long long*)c->tmp.p;
       uint32_t* si = (uint32_t*)vs.sorted_idx.p;
-      void* args[] = {(void*)&r, (void*)&bt, (void*)&be, (void*)&bc, (void*)&scc, (void*)&en, (void*)&tp, (void*)&si};
+      const uint32_t* ht = (const uint32_t*)c->huge_tiles.p;
+      void* args[] = {(void*)&r, (void*)&bt, (void*)&be, (void*)&bc, (void*)&scc, (void*)&en, (void*)&tp, (void*)&si,
+                      (void*)&min_n, (void*)&ht};
       CK(cudaLaunchCooperativeKernel((void*)k_sort_big, c->big_grid, kBigThreadsLarge, args,
                                      (size_t)kBigChunkLarge * 8 + kRadixSmemU32 * 4, s));
     }
@@ -1009,6 +1043,57 @@ int inpc_sort_single64(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   if (F_out) *F_out = F;
   if (sorted_idx && F > 0)
     CK(cudaMemcpyAsync(sorted_idx, va, (size_t)(F < sorted_cap ? F : sorted_cap) * 4, cudaMemcpyDeviceToDevice, s));
+  return INPC_OK;
+}
+
+int inpc_spatial_order(inpc_ctx* c, const float* xyz, int64_t N, uint32_t* perm, void* stream) {
+  if (!c || N < 0) return INPC_INVALID_ARG;
+  if (N > 0xFFFFFFFFll) return INPC_KEY_OVERFLOW;
+  if (N == 0) return INPC_OK;
+  DeviceGuard dg(c->device);
+  if (!is_device_ptr(xyz) || !is_device_ptr(perm)) return INPC_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  c->last_stream = s;
+  cudaGetLastError();
+  AllocScope alloc_scope(c);
+  const int tiles = (int)((N + kRxTile - 1) / kRxTile);
+  const int64_t hist_n = (int64_t)256 * tiles;
+  const int scan_blocks = (int)((hist_n + kScanTile - 1) / kScanTile);
+  bool fresh = false;
+  int st;
+  if ((st = ensure(c->f4_keys, (size_t)N * 8, s))) return st;
+  if ((st = ensure(c->f4_keys2, (size_t)N * 8, s))) return st;
+  if ((st = ensure(c->f4_vals, (size_t)N * 4, s))) return st;
+  if ((st = ensure(c->f4_vals2, (size_t)N * 4, s))) return st;
+  if ((st = ensure(c->f4_hist, (size_t)hist_n * 4, s))) return st;
+  if ((st = ensure(c->f4_scan, (size_t)scan_blocks * 8 + sizeof(ScanCtl) + 16, s, &fresh))) return st;
+  if (fresh) CK(cudaMemsetAsync(c->f4_scan.p, 0, c->f4_scan.bytes, s));
+  if ((st = ensure(c->f4_misc, 64, s))) return st;
+  uint32_t* box = (uint32_t*)c->f4_misc.p;
+  CK(cudaMemsetAsync(box, 0xFF, 12, s));
+  CK(cudaMemsetAsync(box + 3, 0, 12, s));
+  unsigned long long* state = (unsigned long long*)c->f4_scan.p;
+  ScanCtl* ctl = (ScanCtl*)(state + scan_blocks);
+  unsigned long long* ka = (unsigned long long*)c->f4_keys.p;
+  unsigned long long* kb = (unsigned long long*)c->f4_keys2.p;
+  uint32_t* va = (uint32_t*)c->f4_vals.p;
+  uint32_t* vb = (uint32_t*)c->f4_vals2.p;
+  k_aabb<<<c->num_sms * 4, 256, 0, s>>>(xyz, N, box);
+  k_morton_keys<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(xyz, N, box, ka, va);
+  const int rblocks = (tiles + kRxWarps - 1) / kRxWarps;
+  for (int q = 0; q < 4; ++q) {  // 30-bit codes (+ the all-ones code of non-finite points)
+    k_rx_hist<<<rblocks, kRxWarps * 32, 0, s>>>(ka, N, 8 * q, tiles, (uint32_t*)c->f4_hist.p);
+    k_scan_u32<<<scan_blocks, kScanThreads, 0, s>>>(hist_n, (uint32_t*)c->f4_hist.p, state, ctl);
+    k_rx_scatter<<<rblocks, kRxWarps * 32, 0, s>>>(ka, va, N, 8 * q, tiles, (const uint32_t*)c->f4_hist.p, kb, vb);
+    unsigned long long* tk = ka;
+    ka = kb;
+    kb = tk;
+    uint32_t* tv = va;
+    va = vb;
+    vb = tv;
+  }
+  CK(cudaMemcpyAsync(perm, va, (size_t)N * 4, cudaMemcpyDeviceToDevice, s));
+  CK(cudaGetLastError());
   return INPC_OK;
 }
 

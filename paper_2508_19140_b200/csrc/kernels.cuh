@@ -130,8 +130,15 @@ __global__ void __launch_bounds__(256) k_sh_grad(DevCam cam, DevCfg g, const flo
   }
 }
 
-// kPPT points per thread, loads of all of them issued before any compute so
-// enough bytes are in flight to cover HBM latency.
+// kPPT points per thread, the position / opacity loads of all of them issued
+// before any compute so enough bytes are in flight to cover HBM latency.
+// Bilinear with a scatter record (the unfused path of large clouds): the
+// record, the slots and the packed features are touched only for points with
+// a footprint (culled points cost their 16 input bytes and an 8-byte zero
+// scatter record), and the per-(point, tile) slot atomics are aggregated over
+// the lanes of a warp that hit the same tile (__match_any_sync per block
+// corner, one atomicAdd per distinct tile): a spatially ordered cloud puts a
+// warp's 32 consecutive points into a handful of tiles.
 template <int MODE, bool SH>
 __global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
     DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ opacity,
@@ -140,55 +147,107 @@ __global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
     uint32_t* __restrict__ dbg_tiles, float* __restrict__ feat_out, uint2* __restrict__ scat) {
   const int64_t stride = (int64_t)gridDim.x * kPointThreads;
   const int64_t i0 = (int64_t)blockIdx.x * kPointThreads + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  // bilinear + scatter record: visible-only writes, warp-aggregated slots
+  const bool agg = MODE == 0 && scat != nullptr && tile_count != nullptr;
   float X[kPPT], Y[kPPT], Z[kPPT], O[kPPT];
   float4 Fv[kPPT];
 #pragma unroll
   for (int k = 0; k < kPPT; ++k) {
     int64_t i = i0 + k * stride;
+    Fv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i < N) {
       X[k] = __ldg(xyz + 3 * i);
       Y[k] = __ldg(xyz + 3 * i + 1);
       Z[k] = __ldg(xyz + 3 * i + 2);
       O[k] = __ldg(opacity + i);
-      if (MODE == 0 && pack && !SH) Fv[k] = __ldg(reinterpret_cast<const float4*>(feat) + i);
+      if (MODE == 0 && pack && !SH && !agg) Fv[k] = __ldg(reinterpret_cast<const float4*>(feat) + i);
     }
   }
 #pragma unroll
   for (int k = 0; k < kPPT; ++k) {
     int64_t i = i0 + k * stride;
-    if (i >= N) break;
+    if (agg) {
+      if (!__any_sync(0xffffffffu, i < N)) break;  // warp-uniform: the slot collectives need every lane
+    } else if (i >= N) {
+      break;
+    }
+    const bool inr = i < N;
     Proj p;
     Foot f;
     float ca = 0.f, cb = 0.f, cc = 0.f, r = 0.f;
-    bool vis = project_point(cam, X[k], Y[k], Z[k], p);
-    bool ok = false;
-    if (vis) {
-      if (MODE == 0) ok = foot_bilinear(g, p.u, p.v, f);
-      else ok = gauss_conic(cam, g, p, ca, cb, cc, r) && gauss_rect(g, p.u, p.v, r, f);
+    bool vis = false, ok = false;
+    if (inr) {
+      vis = project_point(cam, X[k], Y[k], Z[k], p);
+      if (vis) {
+        if (MODE == 0) ok = foot_bilinear(g, p.u, p.v, f);
+        else ok = gauss_conic(cam, g, p, ca, cb, cc, r) && gauss_rect(g, p.u, p.v, r, f);
+      }
     }
+    if (agg && ok && pack && !SH) Fv[k] = __ldg(reinterpret_cast<const float4*>(feat) + i);
     if (SH && ok) sh_point_features(cam, g, feat, i, X[k], Y[k], Z[k], MODE == 0 && pack, Fv[k], feat_out);
-    PointRec pr;
-    pr.a = make_float4(p.u, p.v, ok ? p.zc : 0.0f, O[k]);
-    if (MODE == 0) pr.b = pack ? Fv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
-    else pr.b = make_float4(ca, cb, cc, r);
-    rec[i] = pr;
-    if (dbg_key) {
+    if (inr && dbg_key) {
       dbg_key[i] = vis ? __float_as_uint(p.zc) : 0xFFFFFFFFu;
       dbg_tiles[i] = ok ? (uint32_t)((f.xhi / kTile - f.xlo / kTile + 1) *
                                      (f.yhi / kTile - f.ylo / kTile + 1))
                         : 0u;
     }
-    if (!ok || !tile_count) {  // tile_count null: records only (f4 baseline)
-      if (MODE == 0 && scat) scat[i] = make_uint2(0u, 0u);
+    if (agg) {
+      // footprint tiles of the 2x2 block (corner c = 2 dy + dx), band-clipped
+      uint32_t tile[4];
+      uint32_t tb = 0u;
+      if (ok) {
+        const int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
+        const int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
+        uint32_t vm = 0u;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int tx = tx_lo + (c & 1), ty = ty_lo + (c >> 1);
+          const bool in = tx <= tx_hi && ty <= ty_hi;
+          tile[c] = in ? (uint32_t)(ty * g.tiles_x + tx) : 0xFFFFFFFFu;
+          vm |= (in ? 1u : 0u) << c;
+        }
+        tb = (uint32_t)(ty_lo * g.tiles_x + tx_lo) | (vm << 28);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tile[c] = 0xFFFFFFFFu;
+      }
+      // all four corners' atomics in flight before any result is used
+      unsigned peers[4];
+      uint32_t base[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        peers[c] = __match_any_sync(0xffffffffu, tile[c]);
+        base[c] = 0u;
+        if (tile[c] != 0xFFFFFFFFu && lane == __ffs(peers[c]) - 1)
+          base[c] = atomicAdd(tile_count + tile[c], (uint32_t)__popc(peers[c]));
+      }
+      if (ok) {
+        PointRec pr;
+        pr.a = make_float4(p.u, p.v, p.zc, O[k]);
+        pr.b = pack ? Fv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+        rec[i] = pr;
+      }
+      uint32_t sl[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t b = __shfl_sync(0xffffffffu, base[c], __ffs(peers[c]) - 1);
+        sl[c] = tile[c] != 0xFFFFFFFFu ? b + (uint32_t)__popc(peers[c] & lt) : 0xFFFFFFFFu;
+      }
+      if (ok) slots[i] = make_uint4(sl[0], sl[1], sl[2], sl[3]);
+      if (inr) scat[i] = ok ? make_uint2(__float_as_uint(p.zc), tb) : make_uint2(0u, 0u);
       continue;
     }
+    PointRec pr;
+    pr.a = make_float4(p.u, p.v, ok ? p.zc : 0.0f, O[k]);
+    if (MODE == 0) pr.b = pack ? Fv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    else pr.b = make_float4(ca, cb, cc, r);
+    rec[i] = pr;
+    if (!ok || !tile_count) continue;  // tile_count null: records only (f4 baseline)
     int ty_lo = max(f.ylo / kTile, g.ty0), ty_hi = min(f.yhi / kTile, g.ty1 - 1);
     int tx_lo = f.xlo / kTile, tx_hi = f.xhi / kTile;
     if (MODE == 0) {
-      // bilinear: <= 4 tiles, corner c = 2 dy + dx of the tile block; the
-      // slot of each entry in its tile is kept so that the scatter needs no
-      // atomics (k_scatter_slots).  Fixed register indices: the atomics of
-      // all corners are in flight together.
       uint32_t sl[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -197,12 +256,6 @@ __global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
                                              : 0xFFFFFFFFu;
       }
       slots[i] = make_uint4(sl[0], sl[1], sl[2], sl[3]);
-      if (scat) {  // what the scatter needs, in 8 bytes: depth key, tile block | corner mask << 28
-        uint32_t vm = 0u;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) vm |= (sl[c] != 0xFFFFFFFFu ? 1u : 0u) << c;
-        scat[i] = make_uint2(__float_as_uint(p.zc), (uint32_t)(ty_lo * g.tiles_x + tx_lo) | (vm << 28));
-      }
     } else {
       for (int ty = ty_lo; ty <= ty_hi; ++ty)
         for (int tx = tx_lo; tx <= tx_hi; ++tx) atomicAdd(tile_count + (size_t)ty * g.tiles_x + tx, 1u);
@@ -223,9 +276,12 @@ __device__ __forceinline__ bool rec_foot(const DevCfg& g, float4 a, float radius
 // before k_scan_tiles).
 struct ViewScalars {
   uint32_t Ft;       // total tile entries
-  uint32_t num_big;  // tiles with more than kWarpSortCap entries (reset by k_sort_big)
+  uint32_t num_big;  // tiles with more than kWarpSortCap entries (reset by k_sort_big / k_sort_mid)
   uint32_t max_big;  // largest of them
   uint32_t pad;      // big-tile chunk dispenser (k_sort_big), zero between calls
+  uint32_t num_huge;  // unfused path: tiles over kMidMax entries (k_sort_big's list; reset by it)
+  uint32_t max_huge;  // largest of them
+  uint32_t pad2, pad3;
 };
 
 // Scan bookkeeping, zero on entry and left zero on exit (the last CTA to
@@ -243,7 +299,8 @@ struct ScanCtl {
 __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
     int T, uint32_t* __restrict__ count, uint32_t* __restrict__ ranges,
     uint32_t* __restrict__ cursor, uint32_t* __restrict__ big_tiles,
-    unsigned long long* state, ScanCtl* ctl, ViewScalars* sc) {
+    unsigned long long* state, ScanCtl* ctl, ViewScalars* sc, uint32_t* __restrict__ huge_tiles,
+    uint32_t huge_min) {
   __shared__ uint32_t warp_tot[kScanThreads / 32];
   __shared__ uint32_t s_prefix, s_bid;
   if (threadIdx.x == 0) s_bid = atomicAdd(&ctl->ticket, 1u);
@@ -322,6 +379,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
       if (c[k] > (uint32_t)kWarpSortCap) {
         big_tiles[atomicAdd(&sc->num_big, 1u)] = i0 + k;
         mx = max(mx, c[k]);
+        if (huge_tiles && c[k] > huge_min) {  // also on k_sort_big's own list
+          huge_tiles[atomicAdd(&sc->num_huge, 1u)] = i0 + k;
+          atomicMax(&sc->max_huge, c[k]);
+        }
       }
     }
     off += c[k];
@@ -440,6 +501,14 @@ __global__ void __launch_bounds__(kPointThreads) k_scatter_slots(
 }
 
 // ---------------------------------------------------------------- sort helpers
+// 8-byte async global->shared copy (LDGSTS): a tile's keys are all in
+// flight at once instead of one load latency per loop iteration.
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all8() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // In-place ascending bitonic sort of np (power of two) 64-bit keys in SMEM by
 // the whole block.
 __device__ __forceinline__ void block_bitonic(unsigned long long* s, int np) {
@@ -744,10 +813,13 @@ __device__ __forceinline__ bool block_sort32_depth(const unsigned long long* s, 
 template <int CHUNK>
 __device__ __forceinline__ void big_sort_body(
     cooperative_groups::grid_group& grid, unsigned long long* s, uint32_t* carry,
-    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles,
-    uint32_t* big_elem, uint32_t* big_chunk, ViewScalars* sc, unsigned long long* entries,
-    unsigned long long* tmp, uint32_t* __restrict__ sorted_idx, uint32_t* radix_smem = nullptr) {
-  const uint32_t nb = *(volatile uint32_t*)&sc->num_big;
+    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles, uint32_t* list_count,
+    uint32_t* list_max, uint32_t* big_elem, uint32_t* big_chunk, ViewScalars* sc, unsigned long long* entries,
+    unsigned long long* tmp, uint32_t* __restrict__ sorted_idx, uint32_t* radix_smem = nullptr,
+    uint32_t min_n = (uint32_t)kWarpSortCap) {
+  // tiles of the big-tile list with at most min_n entries were sorted by
+  // k_sort_mid: they get no chunks here
+  const uint32_t nb = *(volatile uint32_t*)list_count;
   if (nb == 0) return;
   if (blockIdx.x == 0) {
     // exclusive prefixes over the big-tile list (its order is arbitrary; it
@@ -763,7 +835,7 @@ __device__ __forceinline__ void big_sort_body(
       if (j < nb) {
         const uint32_t t = big_tiles[j];
         const uint32_t n = ranges[t + 1] - ranges[t];
-        ch = (n + CHUNK - 1) / CHUNK;
+        ch = n > min_n ? (n + CHUNK - 1) / CHUNK : 0u;
         sz = ch > 1 ? n : 0u;
       }
       uint32_t xs = sz, xc = ch;
@@ -794,7 +866,15 @@ __device__ __forceinline__ void big_sort_body(
   }
   grid.sync();
   BIN_TS(4);
-  const uint32_t total_chunks = big_chunk[nb], total = big_elem[nb], maxn = sc->max_big;
+  const uint32_t total_chunks = big_chunk[nb], total = big_elem[nb], maxn = *list_max;
+  if (total_chunks == 0u) {  // every listed tile was sorted by k_sort_mid (grid-uniform)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // all CTAs read the count before the sync above
+      *list_count = 0u;
+      *list_max = 0u;
+      sc->pad = 0u;
+    }
+    return;
+  }
   // chunks handed out dynamically (sizes vary by tile): carry[0] is this CTA's next chunk
   // (thread 0 draws the chunk and finds its tile: carry = {chunk, list slot})
   if (threadIdx.x == 0) {
@@ -815,13 +895,15 @@ __device__ __forceinline__ void big_sort_body(
     uint32_t* u = radix_smem;                                  // 32-bit keys / permutation
     uint32_t* misc = radix_smem ? radix_smem + 32 * kRadixStride + 32 : nullptr;
     if (radix_smem && n > (uint32_t)kBucketMinN) {
-      for (int k = threadIdx.x; k < (int)n; k += blockDim.x) s[k] = entries[begin + k];
+      for (int k = threadIdx.x; k < (int)n; k += blockDim.x) cp_async8(&s[k], entries + begin + k);
+      cp_async_wait_all8();
       __syncthreads();
       // about 4 buckets per key
       sorted = n > 2048u ? block_bucket_sort<14>(s, (int)n, radix_smem) : block_bucket_sort<13>(s, (int)n, radix_smem);
       if (!sorted && kUseRadix && n > (uint32_t)kRadixMinN) sorted = block_radix_depth(s, (int)n, radix_smem);
     } else if (radix_smem) {
-      for (int k = threadIdx.x; k < (int)n; k += blockDim.x) s[k] = entries[begin + k];
+      for (int k = threadIdx.x; k < (int)n; k += blockDim.x) cp_async8(&s[k], entries + begin + k);
+      cp_async_wait_all8();
       __syncthreads();
       sorted = perm = block_sort32_depth(s, (int)n, np, u, misc);
     }
@@ -886,8 +968,8 @@ __device__ __forceinline__ void big_sort_body(
   }
   grid.sync();  // everybody has read the big-tile counters: zero them for the next call
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    sc->num_big = 0u;
-    sc->max_big = 0u;
+    *list_count = 0u;
+    *list_max = 0u;
     sc->pad = 0u;
   }
 }
@@ -1224,14 +1306,431 @@ __device__ __forceinline__ bool block_sort32_depth(const unsigned long long* s, 
 __global__ void __launch_bounds__(kBigThreadsLarge, INPC_SORT_BIG_MINB) k_sort_big(
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles,
     uint32_t* big_elem, uint32_t* big_chunk, ViewScalars* sc,
-    unsigned long long* entries, unsigned long long* tmp, uint32_t* __restrict__ sorted_idx) {
+    unsigned long long* entries, unsigned long long* tmp, uint32_t* __restrict__ sorted_idx, uint32_t min_n,
+    const uint32_t* __restrict__ huge_tiles) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t carry[2];
   unsigned long long* s = reinterpret_cast<unsigned long long*>(smem_raw);
   uint32_t* rs = reinterpret_cast<uint32_t*>(s + kBigChunkLarge);
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-  big_sort_body<kBigChunkLarge>(grid, s, carry, ranges, big_tiles, big_elem, big_chunk, sc, entries, tmp,
-                                sorted_idx, rs);
+  // huge list (tiles over kMidMax, the rest went through k_sort_mid) or, with
+  // min_n == kWarpSortCap (A/B without k_sort_mid), the whole big-tile list
+  const bool huge = min_n > (uint32_t)kWarpSortCap;
+  big_sort_body<kBigChunkLarge>(grid, s, carry, ranges, huge ? huge_tiles : big_tiles,
+                                huge ? &sc->num_huge : &sc->num_big, huge ? &sc->max_huge : &sc->max_big,
+                                big_elem, big_chunk, sc, entries, tmp, sorted_idx, rs, min_n);
+}
+
+// ---------------------------------------------------------------- H4+H6 mid tiles
+// Tiles of kWarpSortCap + 1 .. kMidMax entries -- the common big tile of the
+// dense clouds (cfg 5: ~800 entries, cfg 4 up to ~7k) -- without
+// the chunk machinery of k_sort_big: one CTA of kMidThreads per tile, the
+// tile's unique 64-bit keys in SMEM, ordered through 32-bit keys
+//   k32 = ((depth bits - tile minimum) >> shift) << slot bits | slot,
+// the depth part truncated to the 32 - slot bits most significant varying
+// bits, by a stable LSD radix sort of 7-bit digits over the varying bits only
+// (three passes for a tile spanning several binades of depth).  Ranking:
+// __match_any_sync per 32-key round of a warp, per-(digit, warp) counters
+// scanned digit-major (stable).  Equal truncated depths stay in slot order;
+// one thread per such run then insertion-sorts it on the full (depth, index)
+// key, so the result is the (depth, index) order bit for bit.  A run longer
+// than kMidMaxRun (many equal depths) falls back to the 64-bit bitonic
+// network.  ~10 thread instructions per key and pass instead of the ~40
+// warp instructions per key of the 1024-thread chunk sorts.
+template <int NT, int MAXN>
+struct MidSort {
+  static constexpr int kWarps = NT / 32;
+  static constexpr int kItems = MAXN / NT;         // keys per thread
+  static constexpr int kSlotBits = MAXN == 2048 ? 11 : MAXN == 4096 ? 12 : 13;
+  static constexpr int kDepthBits = 32 - kSlotBits;
+  static constexpr int kDigitBits = 7;
+  static constexpr int kDigits = 1 << kDigitBits;
+  static constexpr int kCnt = kDigits * kWarps;    // [digit][warp]
+  static constexpr int kCntPerThread = kCnt / NT;
+  static constexpr int kMaxRun = 64;
+  static_assert(MAXN == (1 << kSlotBits), "slot bits");
+  static_assert(kCnt % NT == 0 && (kCntPerThread == 4 || kCntPerThread == 2), "counter layout");
+  struct Smem {
+    unsigned long long s[MAXN];  // full keys, slot order (bitonic fallback: sorted in place)
+    uint32_t k32[MAXN];          // scatter buffer, finally the sorted 32-bit keys
+    __align__(16) uint32_t cnt[kCnt];
+    uint32_t wsum[kWarps];
+    uint32_t red[2][kWarps];
+  };
+};
+constexpr int kMidThreads = 256;
+constexpr int kMidMax = 2048;
+using MidCfg = MidSort<kMidThreads, kMidMax>;
+
+// Sort the n keys of S.s (slot order); returns true with S.k32 holding the
+// sorted 32-bit keys (slot = k32 & (MAXN - 1)), false with S.s itself sorted
+// (bitonic fallback).  Block-uniform result.
+template <int NT, int MAXN>
+__device__ __forceinline__ bool block_radix32(typename MidSort<NT, MAXN>::Smem& S, int n) {
+  using M = MidSort<NT, MAXN>;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+  for (int k = tid; k < n; k += NT) {
+    const uint32_t d = (uint32_t)(S.s[k] >> 32);
+    lo = min(lo, d);
+    hi = max(hi, d);
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if (lane == 0) {
+    S.red[0][w] = lo;
+    S.red[1][w] = hi;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < M::kWarps; ++q) {
+    lo = min(lo, S.red[0][q]);
+    hi = max(hi, S.red[1][q]);
+  }
+  const uint32_t range = hi - lo;
+  const int vbits = range ? 32 - __clz(range) : 0;
+  const int shift = vbits > M::kDepthBits ? vbits - M::kDepthBits : 0;
+  const int npass = (vbits - shift + M::kDigitBits - 1) / M::kDigitBits;
+  const int E = (n + NT - 1) / NT;          // keys per thread (<= kItems)
+  const int wbase = w * 32 * E;
+  uint32_t kv[M::kItems], rk[M::kItems];
+#pragma unroll
+  for (int r = 0; r < M::kItems; ++r) {
+    const int i = wbase + r * 32 + lane;
+    kv[r] = (r < E && i < n) ? ((((uint32_t)(S.s[i] >> 32) - lo) >> shift) << M::kSlotBits) | (uint32_t)i : 0u;
+  }
+  if (npass == 0) {  // one depth: slot order, fixed below
+#pragma unroll
+    for (int r = 0; r < M::kItems; ++r) {
+      const int i = wbase + r * 32 + lane;
+      if (r < E && i < n) S.k32[i] = kv[r];
+    }
+  }
+  for (int p = 0; p < npass; ++p) {
+    const int sh = M::kSlotBits + M::kDigitBits * p;
+    if (M::kCntPerThread == 4) reinterpret_cast<uint4*>(S.cnt)[tid] = make_uint4(0u, 0u, 0u, 0u);
+    else reinterpret_cast<uint2*>(S.cnt)[tid] = make_uint2(0u, 0u);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < M::kItems; ++r) {
+      if (r >= E) break;
+      const int i = wbase + r * 32 + lane;
+      const bool valid = i < n;
+      const uint32_t d = valid ? (kv[r] >> sh) & (uint32_t)(M::kDigits - 1) : (uint32_t)M::kDigits + lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0u;
+      if (valid && lane == leader) {  // only this warp writes column w; one leader per digit and round
+        old = S.cnt[d * M::kWarps + w];
+        S.cnt[d * M::kWarps + w] = old + (uint32_t)__popc(peers);
+      }
+      old = __shfl_sync(0xffffffffu, old, leader);
+      rk[r] = old + (uint32_t)__popc(peers & lt);
+      __syncwarp();
+    }
+    __syncthreads();
+    {  // exclusive scan of the counters in (digit, warp) order
+      uint32_t c[M::kCntPerThread], sum = 0u;
+      if (M::kCntPerThread == 4) {
+        const uint4 v = reinterpret_cast<const uint4*>(S.cnt)[tid];
+        c[0] = v.x; c[1] = v.y; c[M::kCntPerThread > 2 ? 2 : 0] = v.z; c[M::kCntPerThread > 3 ? 3 : 0] = v.w;
+      } else {
+        const uint2 v = reinterpret_cast<const uint2*>(S.cnt)[tid];
+        c[0] = v.x; c[1] = v.y;
+      }
+#pragma unroll
+      for (int q = 0; q < M::kCntPerThread; ++q) sum += c[q];
+      uint32_t x = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) S.wsum[w] = x;
+      __syncthreads();
+      uint32_t run = x - sum;
+      for (int q = 0; q < w; ++q) run += S.wsum[q];
+#pragma unroll
+      for (int q = 0; q < M::kCntPerThread; ++q) {
+        const uint32_t cq = c[q];
+        c[q] = run;
+        run += cq;
+      }
+      if (M::kCntPerThread == 4)
+        reinterpret_cast<uint4*>(S.cnt)[tid] = make_uint4(c[0], c[1], c[M::kCntPerThread > 2 ? 2 : 0],
+                                                         c[M::kCntPerThread > 3 ? 3 : 0]);
+      else
+        reinterpret_cast<uint2*>(S.cnt)[tid] = make_uint2(c[0], c[1]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < M::kItems; ++r) {
+      if (r >= E) break;
+      const int i = wbase + r * 32 + lane;
+      if (i < n) S.k32[S.cnt[((kv[r] >> sh) & (uint32_t)(M::kDigits - 1)) * M::kWarps + w] + rk[r]] = kv[r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < M::kItems; ++r) {
+      if (r >= E) break;
+      const int i = wbase + r * 32 + lane;
+      if (i < n) kv[r] = S.k32[i];
+    }
+  }
+  __syncthreads();
+  // runs of equal truncated depth: (depth, index) order on the full keys
+  constexpr uint32_t smask = (uint32_t)MAXN - 1u;
+  bool bad = false;
+  for (int p = tid; p + 1 < n; p += NT) {
+    const uint32_t a = S.k32[p] >> M::kSlotBits;
+    if ((S.k32[p + 1] >> M::kSlotBits) != a || (p > 0 && (S.k32[p - 1] >> M::kSlotBits) == a)) continue;
+    int end = p + 2;
+    while (end < n && (S.k32[end] >> M::kSlotBits) == a && end - p <= M::kMaxRun) ++end;
+    if (end - p > M::kMaxRun) {
+      bad = true;
+      continue;
+    }
+    for (int k = p + 1; k < end; ++k) {
+      const uint32_t v = S.k32[k];
+      const unsigned long long fv = S.s[v & smask];
+      int j = k - 1;
+      while (j >= p && S.s[S.k32[j] & smask] > fv) {
+        S.k32[j + 1] = S.k32[j];
+        --j;
+      }
+      S.k32[j + 1] = v;
+    }
+  }
+  if (__syncthreads_or(bad)) {
+    int np = 64;
+    while (np < n) np <<= 1;
+    for (int k = n + tid; k < np; k += NT) S.s[k] = ~0ull;
+    __syncthreads();
+    block_bitonic_fast(S.s, np);
+    return false;
+  }
+  return true;
+}
+
+// Warp-level variant for tiles of up to kWarpMidMax entries (the bulk of the
+// mid tiles): one warp sorts one tile alone -- 256 per-warp digit counters
+// (8-bit digits, 10 slot bits, 22 depth bits: three passes), no block
+// barriers, the warp's keys and ranks in registers.
+constexpr int kWarpMidMax = 1024;
+struct WarpMidSmem {
+  unsigned long long s[kWarpMidMax];
+  uint32_t k32[kWarpMidMax];
+  __align__(16) uint32_t cnt[256];
+};
+
+// 64-bit bitonic sort of np (power of two) keys in SMEM by one warp
+// (fallback for long runs of equal depth).
+__device__ __forceinline__ void warp_bitonic_smem(unsigned long long* s, int np, int lane) {
+  for (int k = 2; k <= np; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = lane; t < (np >> 1); t += 32) {
+        const int i = 2 * t - (t & (j - 1));
+        const int ixj = i + j;
+        const unsigned long long a = s[i], b = s[ixj];
+        if ((a > b) == ((i & k) == 0)) {
+          s[i] = b;
+          s[ixj] = a;
+        }
+      }
+      __syncwarp();
+    }
+}
+
+// Sort the n <= kWarpMidMax keys of W.s (slot order) into sorted_idx[0..n).
+__device__ __forceinline__ void warp_radix32_tile(WarpMidSmem& W, int n, uint32_t* __restrict__ out, int lane,
+                                                  int kDepth) {
+  constexpr int kSlot = 10, kDig = 8, kE = kWarpMidMax / 32;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+  for (int k = lane; k < n; k += 32) {
+    const uint32_t d = (uint32_t)(W.s[k] >> 32);
+    lo = min(lo, d);
+    hi = max(hi, d);
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t range = hi - lo;
+  const int vbits = range ? 32 - __clz(range) : 0;
+  const int shift = vbits > kDepth ? vbits - kDepth : 0;
+  const int npass = (vbits - shift + kDig - 1) / kDig;
+  const int E = (n + 31) >> 5;
+  uint32_t kv[kE], rk[kE];
+#pragma unroll
+  for (int r = 0; r < kE; ++r) {
+    const int i = r * 32 + lane;
+    kv[r] = (r < E && i < n) ? ((((uint32_t)(W.s[i] >> 32) - lo) >> shift) << kSlot) | (uint32_t)i : 0u;
+    if (npass == 0 && r < E && i < n) W.k32[i] = kv[r];
+  }
+  for (int p = 0; p < npass; ++p) {
+    const int sh = kSlot + kDig * p;
+    reinterpret_cast<uint4*>(W.cnt)[2 * lane] = make_uint4(0u, 0u, 0u, 0u);
+    reinterpret_cast<uint4*>(W.cnt)[2 * lane + 1] = make_uint4(0u, 0u, 0u, 0u);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) {
+      if (r >= E) break;
+      const bool valid = r * 32 + lane < n;
+      const uint32_t d = valid ? (kv[r] >> sh) & 255u : 256u + lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0u;
+      if (valid && lane == leader) {
+        old = W.cnt[d];
+        W.cnt[d] = old + (uint32_t)__popc(peers);
+      }
+      rk[r] = __shfl_sync(0xffffffffu, old, leader) + (uint32_t)__popc(peers & lt);
+      __syncwarp();
+    }
+    {  // exclusive scan of the 256 counters: lane owns [8 lane, 8 lane + 8)
+      const uint4 a = reinterpret_cast<const uint4*>(W.cnt)[2 * lane];
+      const uint4 b = reinterpret_cast<const uint4*>(W.cnt)[2 * lane + 1];
+      const uint32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t sum = 0u;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sum += c[q];
+      uint32_t x = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      uint32_t e[8], run = x - sum;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        e[q] = run;
+        run += c[q];
+      }
+      __syncwarp();
+      reinterpret_cast<uint4*>(W.cnt)[2 * lane] = make_uint4(e[0], e[1], e[2], e[3]);
+      reinterpret_cast<uint4*>(W.cnt)[2 * lane + 1] = make_uint4(e[4], e[5], e[6], e[7]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) {
+      if (r >= E) break;
+      if (r * 32 + lane < n) W.k32[W.cnt[(kv[r] >> sh) & 255u] + rk[r]] = kv[r];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < kE; ++r) {
+      if (r >= E) break;
+      if (r * 32 + lane < n) kv[r] = W.k32[r * 32 + lane];
+    }
+    __syncwarp();
+  }
+  __syncwarp();
+  constexpr uint32_t smask = (uint32_t)kWarpMidMax - 1u;
+  bool bad = false;
+  for (int p = lane; p + 1 < n; p += 32) {  // runs of equal truncated depth: full-key order
+    const uint32_t a = W.k32[p] >> kSlot;
+    if ((W.k32[p + 1] >> kSlot) != a || (p > 0 && (W.k32[p - 1] >> kSlot) == a)) continue;
+    int end = p + 2;
+    while (end < n && (W.k32[end] >> kSlot) == a && end - p <= MidCfg::kMaxRun) ++end;
+    if (end - p > MidCfg::kMaxRun) {
+      bad = true;
+      continue;
+    }
+    for (int k = p + 1; k < end; ++k) {
+      const uint32_t v = W.k32[k];
+      const unsigned long long fv = W.s[v & smask];
+      int j = k - 1;
+      while (j >= p && W.s[W.k32[j] & smask] > fv) {
+        W.k32[j + 1] = W.k32[j];
+        --j;
+      }
+      W.k32[j + 1] = v;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+    int np = 64;
+    while (np < n) np <<= 1;
+    for (int k = n + lane; k < np; k += 32) W.s[k] = ~0ull;
+    __syncwarp();
+    warp_bitonic_smem(W.s, np, lane);
+    for (int k = lane; k < n; k += 32) out[k] = (uint32_t)W.s[k];
+  } else {
+    __syncwarp();
+    for (int k = lane; k < n; k += 32) out[k] = (uint32_t)W.s[W.k32[k] & smask];
+  }
+  __syncwarp();
+}
+
+// Mid tiles of the big-tile list (kWarpSortCap < n <= kMidMax; larger tiles
+// are left to k_sort_big): first every warp takes tiles of up to
+// kWarpMidMax entries alone (warp-stride over the list), then the CTA sorts
+// the tiles of kWarpMidMax + 1 .. kMidMax entries together (block_radix32).
+constexpr int kSortMidWarps = kMidThreads / 32;
+constexpr size_t kSortMidSmem =
+    sizeof(WarpMidSmem) * kSortMidWarps > sizeof(MidCfg::Smem) ? sizeof(WarpMidSmem) * kSortMidWarps
+                                                                : sizeof(MidCfg::Smem);
+__global__ void __launch_bounds__(kMidThreads) k_sort_mid(const uint32_t* __restrict__ ranges,
+                                                          const uint32_t* __restrict__ big_tiles,
+                                                          const ViewScalars* __restrict__ sc,
+                                                          const unsigned long long* __restrict__ entries,
+                                                          uint32_t* __restrict__ sorted_idx,
+                                                          uint32_t warp_max, int qbits,
+                                                          uint32_t* __restrict__ dispenser) {
+  extern __shared__ __align__(16) unsigned char mid_smem[];
+  const uint32_t nb = sc->num_big;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    WarpMidSmem& W = reinterpret_cast<WarpMidSmem*>(mid_smem)[warp];
+    // tiles handed out one per warp by an atomic dispenser (sizes vary)
+    uint32_t j = 0;
+    if (lane == 0) j = atomicAdd(dispenser, 1u);
+    j = __shfl_sync(0xffffffffu, j, 0);
+    while (j < nb) {
+      const uint32_t t = big_tiles[j];
+      const uint32_t begin = ranges[t], n = ranges[t + 1] - begin;
+      uint32_t jn = 0;
+      if (lane == 0) jn = atomicAdd(dispenser, 1u);
+      if (n <= warp_max) {  // warp-uniform
+        for (int k = lane; k < (int)n; k += 32) cp_async8(&W.s[k], entries + begin + k);
+        cp_async_wait_all8();
+        __syncwarp();
+        warp_radix32_tile(W, (int)n, sorted_idx + begin, lane, qbits);
+      }
+      j = __shfl_sync(0xffffffffu, jn, 0);
+    }
+  }
+  __syncthreads();
+  MidCfg::Smem& S = *reinterpret_cast<MidCfg::Smem*>(mid_smem);
+  for (uint32_t j = blockIdx.x; j < nb; j += gridDim.x) {
+    const uint32_t t = big_tiles[j];
+    const uint32_t begin = ranges[t], n = ranges[t + 1] - begin;
+    if (n <= warp_max || n > (uint32_t)kMidMax) continue;  // block-uniform
+    for (int k = threadIdx.x; k < (int)n; k += kMidThreads) cp_async8(&S.s[k], entries + begin + k);
+    cp_async_wait_all8();
+    __syncthreads();
+    if (block_radix32<kMidThreads, kMidMax>(S, (int)n)) {
+      for (int k = threadIdx.x; k < (int)n; k += kMidThreads)
+        sorted_idx[begin + k] = (uint32_t)S.s[S.k32[k] & (uint32_t)(kMidMax - 1)];
+    } else {
+      for (int k = threadIdx.x; k < (int)n; k += kMidThreads) sorted_idx[begin + k] = (uint32_t)S.s[k];
+    }
+    __syncthreads();
+  }
+  // the last CTA to finish zeroes the dispenser for the next call
+  __shared__ uint32_t s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(dispenser + 1, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {  // every CTA has read the big-tile list count
+    dispenser[0] = 0u;
+    dispenser[1] = 0u;
+    ViewScalars* scw = const_cast<ViewScalars*>(sc);
+    scw->num_big = 0u;
+    scw->max_big = 0u;
+  }
 }
 
 // ---------------------------------------------------------------- H1..H6 fused (bilinear)
@@ -1440,7 +1939,8 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_bin_bilinear(
   grid.sync();
   BIN_TS(3);
   // ---- phase 4: big tiles
-  big_sort_body<kBigChunk>(grid, s, carry, ranges, big_tiles, big_elem, big_chunk, sc, entries, tmp,
+  big_sort_body<kBigChunk>(grid, s, carry, ranges, big_tiles, &sc->num_big, &sc->max_big, big_elem, big_chunk,
+                           sc, entries, tmp,
                            sorted_idx);
   BIN_TS(7);
 }
@@ -1827,7 +2327,9 @@ __global__ void __launch_bounds__(WPB * 32) k_blend_fwd(
     return e < n ? (small ? (uint32_t)S.keys[e] : __ldg(sorted_idx + begin + e)) : 0u;
   };
   constexpr bool pf = PF;
-  uint32_t idx = idx_at(lane);
+  // list indices one chunk ahead of the records (a big tile's indices come
+  // from global memory: the record gathers never wait on them)
+  uint32_t idx = idx_at(lane), idx_nx = idx_at(lane + 32);
   if (pf) prefetch_entry<CMAX>(S.rb, g, rec, feat, packed, idx, lane < n, lane);
   for (uint32_t base = 0; base < n; base += 32) {
     const uint32_t e = base + lane;
@@ -1836,14 +2338,14 @@ __global__ void __launch_bounds__(WPB * 32) k_blend_fwd(
     if (pf) cp_async_wait_all();
     __syncwarp();
     if (e < n) {
-      const EntryRegs r = pf ? entry_from_buf(S.rb, idx, lane)
-                             : load_entry<CMAX>(g, rec, feat, packed, idx_at(e));
+      const EntryRegs r = pf ? entry_from_buf(S.rb, idx, lane) : load_entry<CMAX>(g, rec, feat, packed, idx);
       stage_entry<MODE, CMAX, false>(cs, lane, g, r, feat, packed, tx0, ty0);
     }
     __syncwarp();
-    if (pf && base + 32 < n) {  // the next chunk's records fly while this one is composited
-      idx = idx_at(e + 32);
-      prefetch_entry<CMAX>(S.rb, g, rec, feat, packed, idx, e + 32 < n, lane);
+    if (base + 32 < n) {  // the next chunk's records fly while this one is composited
+      if (pf) prefetch_entry<CMAX>(S.rb, g, rec, feat, packed, idx_nx, e + 32 < n, lane);
+      idx = idx_nx;
+      idx_nx = idx_at(e + 64);
     }
     blend_pixel<MODE, CMAX, COUNT>(cs, g, cs.mask[lane], px, pyA, pcA, base, a);
     blend_pixel<MODE, CMAX, COUNT>(cs, g, cs.mask[lane + 32], px, pyB, pcA + 8, base, b);

@@ -164,33 +164,38 @@ __device__ __forceinline__ float sh_feature(const float* __restrict__ sh, int c,
 }
 
 // ---- NEXT f2: equirectangular environment background (R27).
-// Pixel-centre ray rotated to world space (recomputed: 10 flops instead of
-// the paper's cached direction buffer, 12 B/pixel of HBM on B200);
+// Pixel-centre ray rotated to world space (recomputed: a few flops instead
+// of the paper's cached direction buffer, 12 B/pixel of HBM on B200);
 // u = (atan2(dx, dz)/2pi + 1/2) We, v = acos(dy)/pi He, texel centres at
-// +1/2, bilinear with azimuthal wrap and polar clamp.
+// +1/2, bilinear with azimuthal wrap and polar clamp.  The texel coordinate
+// is computed in fp64: in fp32 a 2048-texel coordinate carries 1.2e-4 texel
+// of rounding (and atan2f another ~1e-4), which on a high-frequency map
+// exceeds the 1e-4 image tolerance; per pixel this is ~100 DP instructions.
 __device__ __forceinline__ void env_weights(const DevCam& c, const DevCfg& g, int px, int py,
                                             int* idx4, float* w4) {
-  const float xc = ((float)px + 0.5f - c.cx) / c.fx, yc = ((float)py + 0.5f - c.cy) / c.fy;
-  const float inv = rsqrtf(xc * xc + yc * yc + 1.0f);
-  float d[3];
+  const double xc = ((double)px + 0.5 - (double)c.cx) / (double)c.fx;
+  const double yc = ((double)py + 0.5 - (double)c.cy) / (double)c.fy;
+  const double inv = 1.0 / sqrt(xc * xc + yc * yc + 1.0);
+  double d[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) d[k] = (c.R[k] * xc + c.R[3 + k] * yc + c.R[6 + k]) * inv;
-  const float PI = 3.14159265358979323846f;
-  const float u = (atan2f(d[0], d[2]) * (0.5f / PI) + 0.5f) * g.env_w;
-  const float v = acosf(fminf(fmaxf(d[1], -1.0f), 1.0f)) * (1.0f / PI) * g.env_h;
-  const float x = u - 0.5f, y = v - 0.5f;
-  const float fx0 = floorf(x), fy0 = floorf(y);
-  const float a = x - fx0, b = y - fy0;
+  for (int k = 0; k < 3; ++k)
+    d[k] = ((double)c.R[k] * xc + (double)c.R[3 + k] * yc + (double)c.R[6 + k]) * inv;
+  const double PI = 3.14159265358979323846;
+  const double u = (atan2(d[0], d[2]) / (2.0 * PI) + 0.5) * g.env_w;
+  const double v = acos(fmin(fmax(d[1], -1.0), 1.0)) / PI * g.env_h;
+  const double x = u - 0.5, y = v - 0.5;
+  const double fx0 = floor(x), fy0 = floor(y);
+  const double a = x - fx0, b = y - fy0;
   int i0 = (int)fx0, j0 = (int)fy0;  // u in [0, We]: x in [-1/2, We - 1/2]
   int i1 = i0 + 1, j1 = j0 + 1;
   i0 = i0 < 0 ? i0 + g.env_w : (i0 >= g.env_w ? i0 - g.env_w : i0);  // azimuthal wrap
   i1 = i1 < 0 ? i1 + g.env_w : (i1 >= g.env_w ? i1 - g.env_w : i1);
   j0 = min(max(j0, 0), g.env_h - 1);
   j1 = min(max(j1, 0), g.env_h - 1);
-  idx4[0] = j0 * g.env_w + i0; w4[0] = (1.0f - a) * (1.0f - b);
-  idx4[1] = j0 * g.env_w + i1; w4[1] = a * (1.0f - b);
-  idx4[2] = j1 * g.env_w + i0; w4[2] = (1.0f - a) * b;
-  idx4[3] = j1 * g.env_w + i1; w4[3] = a * b;
+  idx4[0] = j0 * g.env_w + i0; w4[0] = (float)((1.0 - a) * (1.0 - b));
+  idx4[1] = j0 * g.env_w + i1; w4[1] = (float)(a * (1.0 - b));
+  idx4[2] = j1 * g.env_w + i0; w4[2] = (float)((1.0 - a) * b);
+  idx4[3] = j1 * g.env_w + i1; w4[3] = (float)(a * b);
 }
 
 }  // namespace inpc

@@ -36,6 +36,30 @@ def test_band_split_balanced_and_contiguous():
                 assert max(loads) <= w.sum() / G + w.max() + 1e-6
 
 
+def test_band_split_weight_in_last_rows_keeps_bands_non_empty():
+    """all weight in the last row must not produce empty bands."""
+    for w, G in (([1] * 10 + [30], 4), ([0] * 7 + [1], 8), ([5] + [0] * 20 + [100], 3)):
+        bands = pdist.band_split(w, G)
+        assert bands[0][0] == 0 and bands[-1][1] == len(w)
+        assert all(e > b for b, e in bands), bands
+        assert all(bands[k][1] == bands[k + 1][0] for k in range(G - 1))
+
+
+def test_band_assembler_rows_cover_image():
+    """Row map of the one-call band assembly: every image row exactly once."""
+    import torch
+    H = 67
+    bands = pdist.band_split(np.ones(pdist.tile_rows(H)), 3)
+    asm = pdist.BandAssembler(H, bands, (2,), dtype=torch.float32)
+    rows = asm.rows.numpy()
+    assert len(rows) == H and len(set(rows.tolist())) == H
+    # local emulation of the gather: rank r's slab holds its rows
+    img = torch.arange(H * 2, dtype=torch.float32).view(H, 2)
+    for r in range(3):
+        asm.gathered[r * asm.max_rows:(r + 1) * asm.max_rows] = asm.pack(r, img)
+    assert torch.equal(asm.gathered.index_select(0, asm.rows), img)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -89,18 +113,20 @@ def _views_grads(rank, world):
     pdist.broadcast_cloud([xyz])
     assert np.array_equal(xyz.numpy(), c["xyz"])
 
+    N = c["xyz"].shape[0]
+    flat, gf, go = pdist.flat_grad_buffers(N, 4, dtype=torch.float64)
+
     def local(views):
-        gf = torch.zeros((c["xyz"].shape[0], 4), dtype=torch.float64)
-        go = torch.zeros(c["xyz"].shape[0], dtype=torch.float64)
         for v in views:
             gF, gA, gD = (x[0] for x in synthgen.upstream_grads(v, 1, H, W, 4))
             g = oracle.backward(cams[v], xyz.numpy(), c["feat"], c["opacity"], H, W, gF, gA, gD)
-            gf += torch.from_numpy(g["g_feat"])
-            go += torch.from_numpy(g["g_opacity"])
-        return gf, go
+            gf.add_(torch.from_numpy(g["g_feat"]))
+            go.add_(torch.from_numpy(g["g_opacity"]))
+        return flat
 
-    gf, go = pdist.view_sharded_grads(len(cams), local)
-    return gf.numpy(), go.numpy()
+    out = pdist.view_sharded_grads(len(cams), local)
+    assert out.data_ptr() == flat.data_ptr()       # one all-reduce on the flat buffer, in place
+    return gf.numpy().copy(), go.numpy().copy()
 
 
 def test_view_sharded_gradients_equal_single_process():

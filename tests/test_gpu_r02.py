@@ -1,0 +1,224 @@
+"""Round-2 GPU parity cases (through the C ABI, against the CPU oracle):
+
+  * the bench's launch configuration of the north-star config 5: the static
+    cloud in the library's spatial (Morton) order, which routes the
+    projection through the warp-aggregated slot atomics and the big tiles
+    through k_sort_mid;
+  * non-finite coordinates and points exactly on the near plane (R9) in both
+    binning paths;
+  * the NEXT rows f1 (SH features) and f2 (env-map background,
+    P:185-192) at the size they are benched at (cfg 2, 1080p), sampled;
+  * inpc_spatial_order itself: a permutation, with spatial locality.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synthgen
+from test_gpu_parity import (IMG_TOL, check_grads, check_image, check_lists, dev, gpu_forward,
+                             run_full)
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def inpc():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2508_19140_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(inpc):
+    return inpc.Context(0)
+
+
+@pytest.fixture(scope="module")
+def ctx_unfused(inpc):
+    import os
+    os.environ["INPC_NO_FUSED_BIN"] = "1"
+    try:
+        return inpc.Context(0)
+    finally:
+        del os.environ["INPC_NO_FUSED_BIN"]
+
+
+@pytest.fixture(scope="module")
+def cfg5_spatial(inpc, ctx):
+    """Config 5's cloud in the order bench.py rasterizes it (one-time
+    inpc_spatial_order); the oracle sees the same reordered arrays."""
+    c = synthgen.config5()
+    perm = ctx.spatial_order(dev(c["xyz"])).cpu().numpy()
+    return dict(c, xyz=c["xyz"][perm], feat=c["feat"][perm], opacity=c["opacity"][perm]), perm
+
+
+def test_spatial_order_permutation_and_locality(inpc, ctx, cfg5_spatial):
+    c, perm = cfg5_spatial
+    N = len(perm)
+    assert np.array_equal(np.sort(perm), np.arange(N))
+    a = synthgen.config5()["xyz"].astype(np.float64)
+    step_given = np.linalg.norm(np.diff(a, axis=0), axis=1).mean()
+    step_sorted = np.linalg.norm(np.diff(c["xyz"].astype(np.float64), axis=0), axis=1).mean()
+    assert step_sorted < 0.05 * step_given, (step_sorted, step_given)
+    # non-finite points go last, deterministic across calls
+    x = c["xyz"][:1000].copy()
+    x[7] = np.nan
+    x[11, 2] = np.inf
+    p1 = ctx.spatial_order(dev(x)).cpu().numpy()
+    p2 = ctx.spatial_order(dev(x)).cpu().numpy()
+    assert np.array_equal(p1, p2) and set(p1[-2:].tolist()) == {7, 11}
+
+
+def test_cfg5_spatial_order_bench_configuration(inpc, ctx, cfg5_spatial):
+    """Views 0 and 42 of config 5 in one multi-view call on the spatially
+    ordered cloud: per-view keys, tiles per point and tile lists exact (mid
+    tiles through k_sort_mid), images on sampled pixels, gradients summed over
+    the views against the oracle."""
+    c, _ = cfg5_spatial
+    views = [0, 42]
+    cams = [c["cams"][v] for v in views]
+    H, W, C = c["H"], c["W"], c["C"]
+    N = c["xyz"].shape[0]
+    cfg = inpc.make_cfg(H, W, C, flags=inpc.FLAG_DEBUG)
+    xyz, feat, op = dev(c["xyz"]), dev(c["feat"]), dev(c["opacity"])
+    out = ctx.forward(cfg, cams, xyz, feat, op, debug_counts=True)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(50)
+    masks = []
+    for k, cam in enumerate(cams):
+        ex = ctx.debug_export(k, N=N, H=H, W=W)
+        info = oracle.point_info(cam, c["xyz"], H, W)
+        np.testing.assert_array_equal(ex["depth_keys"].cpu().numpy().view(np.uint32), info["depth_key"])
+        np.testing.assert_array_equal(ex["tiles_touched"].cpu().numpy().view(np.uint32), info["tiles_touched"])
+        tr, ti = oracle.tile_lists(cam, c["xyz"], H, W)
+        np.testing.assert_array_equal(ex["tile_ranges"].cpu().numpy().view(np.uint32), tr)
+        np.testing.assert_array_equal(ex["sorted_idx"].cpu().numpy().view(np.uint32), ti)
+        n = np.diff(tr.astype(np.int64))
+        assert ((n > 256) & (n <= 2048)).sum() > 1000     # the mid-tile sort is exercised
+        mask = rng.random((H, W)) < 0.01
+        for t in rng.integers(0, 32400, 30):              # + whole tiles
+            ty, tx = divmod(int(t), 240)
+            mask[ty * 8:(ty + 1) * 8, tx * 8:(tx + 1) * 8] = True
+        masks.append(mask)
+        r = oracle.render(cam, c["xyz"], c["feat"], c["opacity"], H, W, pixel_mask=mask,
+                          threads=oracle.max_threads())
+        np.testing.assert_array_equal(out["nfrag"][k].cpu().numpy()[mask], r["n_frag"][mask])
+        np.testing.assert_array_equal(out["ncontrib"][k].cpu().numpy()[mask], r["n_contrib"][mask])
+        for key in ("F", "A", "D"):
+            np.testing.assert_allclose(out[key][k].cpu().numpy()[mask], r[key][mask], atol=IMG_TOL)
+    gF, gA, gD = synthgen.upstream_grads(19, len(views), H, W, C)
+    for k, m in enumerate(masks):
+        gF[k] *= m[..., None]; gA[k] *= m; gD[k] *= m
+    gf, go = ctx.backward(cfg, cams, xyz, feat, op, dev(gF), dev(gA), dev(gD))
+    torch.cuda.synchronize()
+    gfo = np.zeros((N, C)); goo = np.zeros(N)
+    for k, cam in enumerate(cams):
+        o = oracle.backward(cam, c["xyz"], c["feat"], c["opacity"], H, W, gF[k], gA[k], gD[k],
+                            pixel_mask=masks[k], threads=oracle.max_threads())
+        gfo += o["g_feat"]; goo += o["g_opacity"]
+    check_grads(gf.cpu().numpy(), gfo)
+    check_grads(go.cpu().numpy(), goo)
+
+
+def _nonfinite_case(seed=3):
+    c = synthgen.config1(seed=seed)
+    xyz = c["xyz"].copy()
+    z_near = np.float32(c["cams"][0]["z_near"])
+    xyz[0] = [np.nan, 0.0, 2.0]
+    xyz[1] = [0.0, np.inf, 2.0]
+    xyz[2] = [0.1, 0.1, -np.inf]
+    xyz[3] = [0.0, 0.0, np.nan]
+    xyz[4] = [np.inf, -np.inf, np.inf]
+    xyz[5] = [0.0, 0.0, z_near]                                  # on the near plane: culled (R9)
+    xyz[6] = [0.0, 0.0, np.nextafter(z_near, np.float32(1))]     # just in front: kept, huge footprint offset
+    xyz[7] = [0.001, -0.002, np.nextafter(z_near, np.float32(1))]
+    xyz[8] = [3e38, 3e38, 1.0]                                   # finite, projects off image
+    return dict(c, xyz=xyz)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_nonfinite_and_near_plane_points(inpc, ctx, ctx_unfused, fused):
+    c = _nonfinite_case()
+    res = run_full(inpc, ctx if fused else ctx_unfused, c)
+    keys = res["depth_keys"][:9]
+    assert list(keys[:6]) == [0xFFFFFFFF] * 6
+    assert keys[6] != 0xFFFFFFFF and keys[7] != 0xFFFFFFFF
+
+
+def test_sh_features_at_bench_size_sampled(inpc, ctx):
+    """f1 at cfg 2 size (2^20 points, 1080p, C = 4 x 9 coefficients), the
+    configuration `bench.py --config 2 --variant sh` times: lists exact,
+    image on sampled pixels against the oracle fed with oracle-evaluated
+    features, coefficient gradients on the points of the sampled pixels."""
+    c = synthgen.config2()
+    H, W, C = c["H"], c["W"], c["C"]
+    N = c["xyz"].shape[0]
+    cam = c["cams"][0]
+    sh = np.random.default_rng(13).normal(0, 0.5, (N, C, 9)).astype(np.float32)
+    f_or, Y = oracle.sh_features(cam, c["xyz"], sh)
+    cfg = inpc.make_cfg(H, W, C, flags=inpc.FLAG_SH_FEATURES | inpc.FLAG_DEBUG)
+    xyz, op, sht = dev(c["xyz"]), dev(c["opacity"]), dev(sh)
+    out = ctx.forward(cfg, c["cams"], xyz, sht, op, debug_counts=True)
+    torch.cuda.synchronize()
+    ex = ctx.debug_export(0, N=N, H=H, W=W)
+    tr, ti = oracle.tile_lists(cam, c["xyz"], H, W)
+    np.testing.assert_array_equal(ex["sorted_idx"].cpu().numpy().view(np.uint32), ti)
+    mask = np.random.default_rng(14).random((H, W)) < 0.02
+    r = oracle.render(cam, c["xyz"], f_or, c["opacity"], H, W, pixel_mask=mask, threads=oracle.max_threads())
+    ok = out["ncontrib"][0].cpu().numpy()[mask] == r["n_contrib"][mask]
+    assert (~ok).sum() <= 2        # SH values are fp32 on the GPU, fp64 in the oracle (R26)
+    np.testing.assert_allclose(out["F"][0].cpu().numpy()[mask][ok], r["F"][mask][ok], atol=IMG_TOL)
+    gF, gA, gD = (x[0] for x in synthgen.upstream_grads(15, 1, H, W, C))
+    gF *= mask[..., None]; gA *= mask; gD *= mask
+    gsh, go = ctx.backward(cfg, c["cams"], xyz, sht, op, dev(gF), dev(gA), dev(gD))
+    torch.cuda.synchronize()
+    o = oracle.backward(cam, c["xyz"], f_or, c["opacity"], H, W, gF, gA, gD, pixel_mask=mask,
+                        threads=oracle.max_threads())
+    check_grads(gsh.cpu().numpy(), o["g_feat"][:, :, None] * Y[:, None, :])
+    check_grads(go.cpu().numpy(), o["g_opacity"])
+
+
+def test_env_background_at_bench_size_sampled(inpc, ctx):
+    """f2 at cfg 2 size with the paper's 1024 x 2048 map, the
+    configuration `bench.py --config 2 --variant env` times."""
+    c = synthgen.config2()
+    H, W, C = c["H"], c["W"], c["C"]
+    cam = c["cams"][0]
+    env = np.random.default_rng(16).uniform(-1, 1, (1024, 2048, C)).astype(np.float32)
+    mask = np.random.default_rng(17).random((H, W)) < 0.02
+    bg = oracle.env_background(cam, env, H, W)
+    cfg = inpc.make_cfg(H, W, C, env_hw=env.shape[:2], flags=inpc.FLAG_DEBUG)
+    xyz, feat, op, envt = dev(c["xyz"]), dev(c["feat"]), dev(c["opacity"]), dev(env)
+    out = ctx.forward(cfg, c["cams"], xyz, feat, op, bg=envt, debug_counts=True)
+    torch.cuda.synchronize()
+    r = oracle.render(cam, c["xyz"], c["feat"], c["opacity"], H, W, bg=bg, pixel_mask=mask,
+                      threads=oracle.max_threads())
+    np.testing.assert_array_equal(out["ncontrib"][0].cpu().numpy()[mask], r["n_contrib"][mask])
+    np.testing.assert_allclose(out["F"][0].cpu().numpy()[mask], r["F"][mask], atol=IMG_TOL)
+    gF, gA, gD = (x[0] for x in synthgen.upstream_grads(18, 1, H, W, C))
+    gF *= mask[..., None]; gA *= mask; gD *= mask
+    gf, go = ctx.backward(cfg, c["cams"], xyz, feat, op, dev(gF), dev(gA), dev(gD), bg=envt)
+    torch.cuda.synchronize()
+    o = oracle.backward(cam, c["xyz"], c["feat"], c["opacity"], H, W, gF, gA, gD, bg=bg, pixel_mask=mask,
+                        threads=oracle.max_threads())
+    check_grads(gf.cpu().numpy(), o["g_feat"])
+    check_grads(go.cpu().numpy(), o["g_opacity"])
+
+
+def test_cfg4_spatial_order_sampled(inpc, ctx):
+    """Config 4 (2^25 points) in the spatial order bench.py uses: keys, tile
+    lists exact (k_sort_mid + k_sort_big), image on sampled pixels."""
+    c = synthgen.config4()
+    perm = ctx.spatial_order(dev(c["xyz"])).cpu().numpy()
+    c = dict(c, xyz=c["xyz"][perm], feat=c["feat"][perm], opacity=c["opacity"][perm])
+    cfg, _, res = gpu_forward(inpc, ctx, c, "bilinear")
+    check_lists(c, res, "bilinear")
+    H, W = c["H"], c["W"]
+    rng = np.random.default_rng(44)
+    mask = rng.random((H, W)) < 0.02
+    for t in rng.integers(0, 32400, 40):
+        ty, tx = divmod(int(t), 240)
+        mask[ty * 8:(ty + 1) * 8, tx * 8:(tx + 1) * 8] = True
+    check_image(c, res, "bilinear", pixel_mask=mask)

@@ -28,7 +28,7 @@ for row in raw[2:]:
 
 names = sorted({r[h.index("Kernel Name")] for r in raw[2:]})
 for n in names:
-    short = n.split("(")[0]
+    short = n.split("(")[0].replace("void ", "")
     src = list(csv.reader(ncu("--page", "source", "--csv", "--kernel-name", "regex:" + short.split("::")[-1].split("<")[0]).splitlines()))
     if len(src) < 3:
         continue
