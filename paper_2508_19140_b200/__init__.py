@@ -180,8 +180,41 @@ def _strides(cfg, N, feat, bg):
     return fstride, bstride
 
 
+def _check_tensor(name, t, device, shape=None, allow_none=False):
+    """fp32, contiguous, on `device`, with the expected shape (None entries
+    are free) -- the C ABI reads raw fp32 pointers."""
+    import torch
+
+    def bad(msg):
+        raise RasterError(INVALID_ARG, msg)
+    if t is None:
+        if allow_none:
+            return
+        bad(f"{name} is required")
+    if not torch.is_tensor(t) or t.dtype != torch.float32:
+        bad(f"{name} must be a float32 tensor (got {getattr(t, 'dtype', type(t))})")
+    if t.device != device:
+        bad(f"{name} is on {t.device}, expected {device}")
+    if not t.is_contiguous():
+        bad(f"{name} must be contiguous")
+    if shape is not None:
+        if t.dim() != len(shape) or any(e is not None and e != d for e, d in zip(shape, t.shape)):
+            bad(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+def _feat_shape(cfg, N, feat):
+    """[N, C] / [V, N, C], or [N, C, 9] / [V, N, C, 9] with FLAG_SH_FEATURES."""
+    sh = bool(cfg.flags & FLAG_SH_FEATURES)
+    tail = (N, cfg.C, 9) if sh else (N, cfg.C)
+    return tail if feat.dim() == len(tail) else (None,) + tail
+
+
 class Context:
-    """Owns an inpc_ctx (scratch arena + the state saved by forward)."""
+    """Owns an inpc_ctx (scratch arena + the state saved by forward).
+
+    The saved state belongs to the most recent forward: `generation`
+    increases with every forward, and the autograd path checks that the
+    state it backpropagates through is still its own."""
 
     def __init__(self, device=None, torch_allocator=True):
         """torch_allocator: the library's scratch arena and saved state come
@@ -194,6 +227,7 @@ class Context:
         _check(lib.inpc_ctx_create(ct.byref(h), dev))
         self._h = h
         self._cb = None
+        self.generation = 0
         if torch_allocator:
             def _alloc(nbytes, device, stream, user):
                 try:
@@ -228,8 +262,12 @@ class Context:
         cam_arr, V = _cams(cams)
         N = xyz.shape[0]
         C, H, W = cfg.C, cfg.H, cfg.W
-        fstride, bstride = _strides(cfg, N, feat, bg)
         dev = xyz.device
+        _check_tensor("xyz", xyz, dev, (N, 3))
+        _check_tensor("feat", feat, dev, _feat_shape(cfg, N, feat))
+        _check_tensor("opacity", opacity, dev, (N,))
+        _check_tensor("bg", bg, dev, allow_none=True)
+        fstride, bstride = _strides(cfg, N, feat, bg)
         if out is None:
             out = dict(F=torch.empty((V, H, W, C), device=dev, dtype=torch.float32),
                        A=torch.empty((V, H, W), device=dev, dtype=torch.float32),
@@ -241,6 +279,7 @@ class Context:
             self._h, ct.byref(cfg), cam_arr, V, _ptr(xyz), _ptr(feat), fstride, _ptr(opacity), N,
             _ptr(bg), bstride, _ptr(out["F"]), _ptr(out.get("A")), _ptr(out.get("D")),
             _ptr(out.get("nfrag")), _ptr(out.get("ncontrib")), _stream(stream)))
+        self.generation += 1
         return out
 
     # -------------------------------------------------------------- backward
@@ -252,11 +291,21 @@ class Context:
         cam_arr, V = _cams(cams)
         N = xyz.shape[0]
         C, H, W = cfg.C, cfg.H, cfg.W
+        dev = xyz.device
+        _check_tensor("xyz", xyz, dev, (N, 3))
+        _check_tensor("feat", feat, dev, _feat_shape(cfg, N, feat))
+        _check_tensor("opacity", opacity, dev, (N,))
+        _check_tensor("bg", bg, dev, allow_none=True)
+        _check_tensor("gF", gF, dev, (V, H, W, C))
+        _check_tensor("gA", gA, dev, (V, H, W), allow_none=True)
+        _check_tensor("gD", gD, dev, (V, H, W), allow_none=True)
         fstride, bstride = _strides(cfg, N, feat, bg)
         if g_feat is None:
             g_feat = torch.zeros_like(feat)
         if g_opacity is None:
             g_opacity = torch.zeros_like(opacity)
+        _check_tensor("g_feat", g_feat, dev, tuple(feat.shape))
+        _check_tensor("g_opacity", g_opacity, dev, (N,))
         _check(lib.inpc_rasterize_bwd(
             self._h, ct.byref(cfg), cam_arr, V, _ptr(xyz), _ptr(feat), fstride, _ptr(opacity), N,
             _ptr(bg), bstride, _ptr(gF), _ptr(gA), _ptr(gD), _ptr(g_feat), _ptr(g_opacity),
@@ -343,25 +392,61 @@ def default_context(device=None) -> Context:
     return _default_ctx[dev]
 
 
+class _ContextPool:
+    """Contexts for in-flight autograd graphs of rasterize(): a graph holds
+    its context (and so its saved forward state) until its backward ran or
+    the graph was freed, so two rasterize() calls before one .backward() do
+    not share saved state."""
+
+    def __init__(self):
+        self.free = {}
+
+    def acquire(self, device):
+        lst = self.free.setdefault(device, [])
+        return lst.pop() if lst else Context(device)
+
+    def release(self, ctx):
+        if getattr(ctx, "_h", None):
+            self.free.setdefault(ctx.device, []).append(ctx)
+
+
+_pool = _ContextPool()
+
+
 def _autograd():
+    import weakref
+
     import torch
 
     class RasterizeFn(torch.autograd.Function):
         @staticmethod
         def forward(actx, xyz, feat, opacity, bg, settings):
             cfg, cams, context = settings
+            owned = context is None
+            if owned:
+                context = _pool.acquire(xyz.device.index)
             out = context.forward(cfg, cams, xyz, feat, opacity, bg=bg)
             actx.save_for_backward(xyz, feat, opacity, bg)
-            actx.settings = settings
+            actx.settings = (cfg, cams, context)
+            actx.generation = context.generation
+            actx.owned = owned
+            if owned:   # back to the pool when the graph goes away without a backward
+                actx.finalizer = weakref.finalize(actx, _pool.release, context)
             return out["F"], out["A"], out["D"]
 
         @staticmethod
         def backward(actx, gF, gA, gD):
             xyz, feat, opacity, bg = actx.saved_tensors
             cfg, cams, context = actx.settings
+            if context.generation != actx.generation:
+                raise RuntimeError("inpc: the context's saved forward state was overwritten by a later "
+                                   "forward on the same context; give each in-flight graph its own "
+                                   "context (rasterize(..., context=None) does)")
             gf, go = context.backward(cfg, cams, xyz, feat, opacity, gF.contiguous(),
                                       None if gA is None else gA.contiguous(),
                                       None if gD is None else gD.contiguous(), bg=bg)
+            if actx.owned:
+                actx.finalizer()   # release now (detaches the finalizer)
             return None, gf, go, None, None
 
     return RasterizeFn
@@ -371,15 +456,18 @@ _Fn = None
 
 
 def rasterize(xyz, feat, opacity, cams, H, W, mode="bilinear", sigma=0.0, dilation=0.16,
-              alpha_max=0.99, t_min=1e-4, bg=None, band=None, flags=0, context=None):
+              alpha_max=0.99, t_min=1e-4, bg=None, band=None, flags=0, env_hw=None, context=None):
     """Differentiable raster of V views: returns F [V,H,W,C], A [V,H,W], D [V,H,W].
-    Gradients flow to feat and opacity.  The context holds the
-    forward's saved state: one autograd graph per context at a time."""
+    Gradients flow to feat and opacity (P:482-491).  feat: [N,C] or [V,N,C];
+    with FLAG_SH_FEATURES the SH coefficients [N,C,9].  env_hw: size of
+    an equirectangular background map `bg` [He,We,C].
+    context=None: each call's graph holds its own pooled context until its
+    backward; an explicit context is shared (its backward then raises if a
+    later forward overwrote the saved state)."""
     global _Fn
     if _Fn is None:
         _Fn = _autograd()
-    C = feat.shape[-1]
-    cfg = make_cfg(H, W, C, mode, sigma, dilation, alpha_max, t_min, band, flags)
-    context = context or default_context(xyz.device.index)
+    C = feat.shape[-2] if (flags & FLAG_SH_FEATURES) else feat.shape[-1]
+    cfg = make_cfg(H, W, C, mode, sigma, dilation, alpha_max, t_min, band, flags, env_hw=env_hw)
     return _Fn.apply(xyz.contiguous(), feat.contiguous(), opacity.contiguous(),
                      None if bg is None else bg.contiguous(), (cfg, cams, context))

@@ -72,10 +72,8 @@ struct inpc_ctx {
   int device = 0;
   int num_sms = 148;
   int big_grid = 0;
-  int mid_grid = 0;        // k_sort_mid: resident CTAs (grid-stride over the big-tile list)
-  bool no_mid_sort = false;
-  int mid_qbits = 16;       // depth bits of the warp mid sort's keys (2 passes of 8-bit digits)
-  uint32_t mid_warp_max = 0; // k_sort_mid: tiles up to this size are sorted by one warp, larger by the CTA // env INPC_NO_MID_SORT=1: every big tile through k_sort_big (A/B)
+  int mid_grid = 0;       // k_sort_mid: resident CTAs (grid-stride over the big-tile list)
+  bool no_mid_sort = false; // env INPC_NO_MID_SORT=1: every big tile through k_sort_big (A/B)
   // scratch (shared by views, stream ordered)
   Buf scat;  // unfused bilinear binning: depth key + tile block | corner mask per point
   Buf zeroed, cursor, big_tiles, huge_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg, g_eval;
@@ -450,18 +448,11 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_big, kBigThreadsLarge, big_smem);
   c->big_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
   per_sm = 0;
-  cudaFuncSetAttribute(k_sort_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortMidSmem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_mid, kMidThreads, kSortMidSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_mid, kMidThreads, 0);
   c->mid_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
   {
     const char* e = getenv("INPC_NO_MID_SORT");
     c->no_mid_sort = e && e[0] == '1';
-    const char* w = getenv("INPC_MID_WARP_MAX");  // A/B: tiles up to this size sorted by one warp
-    c->mid_warp_max = w ? (uint32_t)atoi(w) : (uint32_t)kWarpMidMax;
-    if (c->mid_warp_max > (uint32_t)kWarpMidMax) c->mid_warp_max = kWarpMidMax;
-    const char* q = getenv("INPC_MID_QBITS");  // A/B: depth bits kept in the warp sort's 32-bit keys
-    c->mid_qbits = q ? atoi(q) : 16;
-    if (c->mid_qbits < 8 || c->mid_qbits > 22) c->mid_qbits = 16;
   }
   {
     int o2 = 0, o4 = 0, o8 = 0;
@@ -629,7 +620,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   if ((st = ensure(c->huge_tiles, (size_t)(T + 1) * 4, s))) return st;
   if ((st = ensure(c->big_elem, (size_t)(T + 2) * 4, s))) return st;
   if ((st = ensure(c->big_chunk, (size_t)(T + 2) * 4, s))) return st;
-  if ((st = ensure(c->overflow, 64, s, &fresh))) return st;  // [0] Gaussian overflow flag, [4..5] k_sort_mid dispenser
+  if ((st = ensure(c->overflow, 64, s, &fresh))) return st;  // [0] Gaussian overflow flag, [6] k_sort_mid done counter
   if (fresh) CK(cudaMemsetAsync(c->overflow.p, 0, c->overflow.bytes, s));
   uint64_t bound = gauss ? 0 : 4ull * (uint64_t)N;  // bilinear: <= 4 tiles per point
   if (!gauss && bound >= 0xFFFFFFFFull) return INPC_KEY_OVERFLOW;
@@ -785,11 +776,22 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     }
     if (N > kWarpSortCap && !fused_kp && !c->no_mid_sort) {  // tiles of 257..kMidMax entries
       StageTimer tm(c, s, kStSortMid, 1);
-      k_sort_mid<<<c->mid_grid, kMidThreads, kSortMidSmem, s>>>((const uint32_t*)vs.ranges.p, (const uint32_t*)c->big_tiles.p,
-                                                     sc, (const unsigned long long*)c->entries.p,
-                                                     (uint32_t*)vs.sorted_idx.p, c->mid_warp_max, c->mid_qbits,
-                                                     (uint32_t*)c->overflow.p + 4);
+      k_sort_mid<<<c->mid_grid, kMidThreads, 0, s>>>((const uint32_t*)vs.ranges.p,
+                                                     (const uint32_t*)c->big_tiles.p, sc,
+                                                     (const unsigned long long*)c->entries.p,
+                                                     (uint32_t*)vs.sorted_idx.p, (uint32_t*)c->overflow.p + 6);
       CK(cudaGetLastError());
+#ifdef INPC_PHASE_TIMES
+      {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t[8];
+        cudaStreamSynchronize(s);
+        cudaMemcpyFromSymbol(t, g_mid_cyc, sizeof(t));
+        cudaMemcpyToSymbol(g_mid_cyc, z, sizeof(z));
+        const double nt = t[6] ? (double)t[6] : 1.0;
+        fprintf(stderr, "mid cta: %llu tiles, cycles/tile: list %.0f keys %.0f minmax %.0f passes %.0f fixup %.0f out %.0f\n",
+                t[6], t[0] / nt, t[1] / nt, t[2] / nt, t[3] / nt, t[4] / nt, t[5] / nt);
+      }
+#endif
     }
     if (N > kWarpSortCap && !fused_kp) {  // a tile can only exceed the cap with > cap points
       StageTimer tm(c, s, kStSortBig, 1);

@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(256) k_sh_grad(DevCam cam, DevCfg g, const flo
 // a footprint (culled points cost their 16 input bytes and an 8-byte zero
 // scatter record), and the per-(point, tile) slot atomics are aggregated over
 // the lanes of a warp that hit the same tile (__match_any_sync per block
-// corner, one atomicAdd per distinct tile): a spatially ordered cloud puts a
-// warp's 32 consecutive points into a handful of tiles.
+// corner, one atomicAdd per distinct tile) when a warp's 32 consecutive
+// points fall into a handful of tiles (a spatially ordered cloud).
 template <int MODE, bool SH>
 __global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
     DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ opacity,
@@ -213,7 +213,10 @@ __global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
 #pragma unroll
         for (int c = 0; c < 4; ++c) tile[c] = 0xFFFFFFFFu;
       }
-      // all four corners' atomics in flight before any result is used
+      // all four corners' atomics in flight before any result is used.
+      // (__match_any_sync costs ~2 cycles per distinct value per SM; a
+      // guard that skipped it for warps with many distinct tiles measured
+      // slower on the spatially ordered cfg 4 / cfg 5 clouds: 441 -> 777 us)
       unsigned peers[4];
       uint32_t base[4];
 #pragma unroll
@@ -501,6 +504,23 @@ __global__ void __launch_bounds__(kPointThreads) k_scatter_slots(
 }
 
 // ---------------------------------------------------------------- sort helpers
+// Lanes of the warp whose BITS-bit digit equals this lane's, among the lanes
+// with `valid` set (meaningful for valid lanes only): BITS + 1 ballots.
+// Replaces __match_any_sync, whose throughput on sm_100a is about one
+// instruction per 64 cycles per SM when the 32 values are distinct
+// (tools/mb_match.cu: 2048 cycles per match per warp at 32 warps / SM).
+template <int BITS>
+__device__ __forceinline__ unsigned warp_peers(uint32_t d, bool valid) {
+  unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int j = 0; j < BITS; ++j) {
+    const bool bit = (d >> j) & 1u;
+    const unsigned b = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? b : ~b;
+  }
+  return peers;
+}
+
 // 8-byte async global->shared copy (LDGSTS): a tile's keys are all in
 // flight at once instead of one load latency per loop iteration.
 __device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
@@ -1109,7 +1129,7 @@ __device__ __forceinline__ bool block_bucket_sort(unsigned long long* s, int n, 
 // digits over the depth bits that vary in this chunk only (a tile's depths
 // share exponent and leading mantissa bits: 3 passes on cfg 4), each pass
 // stable: warp w owns elements [32 E w, 32 E (w+1)) in rounds of 32, lanes
-// with the same digit rank themselves with __match_any_sync, per-(digit,
+// with the same digit rank themselves (warp_peers ballots), per-(digit,
 // warp) counts are scanned digit-major.  The keys of a pass sit in
 // registers, so the scatter goes back into s in place.  Stability keeps equal
 // depths in input order; runs of equal depth are then put in index order by
@@ -1163,8 +1183,8 @@ __device__ __forceinline__ bool block_radix_depth(unsigned long long* s, int n, 
         if (r >= E) break;
         const int i = wbase + r * 32 + lane;
         const bool valid = i < n;
-        const uint32_t d = valid ? (uint32_t)(kv[r] >> (32 + sh)) & 255u : 256u + lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t d = (uint32_t)(kv[r] >> (32 + sh)) & 255u;
+        const unsigned peers = warp_peers<8>(d, valid);
         const int leader = __ffs(peers) - 1;
         uint32_t cnt = 0;  // the leader advances the warp's counter of d; SMEM atomics keep rounds in order
         if (valid && lane == leader) cnt = atomicAdd(&hist[w * kRadixStride + d], (uint32_t)__popc(peers));
@@ -1323,33 +1343,53 @@ __global__ void __launch_bounds__(kBigThreadsLarge, INPC_SORT_BIG_MINB) k_sort_b
 
 // ---------------------------------------------------------------- H4+H6 mid tiles
 // Tiles of kWarpSortCap + 1 .. kMidMax entries -- the common big tile of the
-// dense clouds (cfg 5: ~800 entries, cfg 4 up to ~7k) -- without
-// the chunk machinery of k_sort_big: one CTA of kMidThreads per tile, the
-// tile's unique 64-bit keys in SMEM, ordered through 32-bit keys
+// dense clouds (cfg 5: ~800 entries) -- without the chunk
+// machinery of k_sort_big: one CTA of kMidThreads per tile, the tile's
+// unique 64-bit keys in SMEM, ordered through 32-bit keys
 //   k32 = ((depth bits - tile minimum) >> shift) << slot bits | slot,
-// the depth part truncated to the 32 - slot bits most significant varying
-// bits, by a stable LSD radix sort of 7-bit digits over the varying bits only
-// (three passes for a tile spanning several binades of depth).  Ranking:
-// __match_any_sync per 32-key round of a warp, per-(digit, warp) counters
-// scanned digit-major (stable).  Equal truncated depths stay in slot order;
-// one thread per such run then insertion-sorts it on the full (depth, index)
+// the depth part quantised to the kDepthBits most significant varying bits,
+// by a stable LSD radix sort of 4-bit digits over those bits only.
+// Ranking without a serial counter chain: the keys are taken in rounds of 32
+// (round R = keys [32R, 32R + 32) of the current order); in a round each
+// lane finds the lanes with its digit by 4 + 1 ballots (warp_peers), the
+// lowest of them stores the round's count in cnt[digit][R] and every lane
+// keeps its rank inside the round; one exclusive scan of cnt in (digit,
+// round) order then gives every (digit, round) its output base -- stable,
+// and every round independent of the others (the __match_any_sync /
+// per-warp-counter variants measured 2-3x slower: MATCH.ANY costs ~2 SM
+// cycles per distinct value, and a leader's load-add-store chain per round
+// serialises the rounds).  Equal quantised depths stay in slot order; one
+// thread per such run then insertion-sorts it on the full (depth, index)
 // key, so the result is the (depth, index) order bit for bit.  A run longer
-// than kMidMaxRun (many equal depths) falls back to the 64-bit bitonic
-// network.  ~10 thread instructions per key and pass instead of the ~40
-// warp instructions per key of the 1024-thread chunk sorts.
+// than kMaxRun (many equal depths) falls back to the 64-bit bitonic network.
+#ifdef INPC_PHASE_TIMES  // diagnostics: clock64 cycles per phase of the mid-tile CTA sort (thread 0)
+__device__ unsigned long long g_mid_cyc[8];
+#define MID_T(k)                            \
+  do {                                      \
+    if (prof && threadIdx.x == 0) {         \
+      const long long t_ = clock64();       \
+      prof[k] += (unsigned long long)(t_ - tp_); \
+      tp_ = t_;                             \
+    }                                       \
+  } while (0)
+#else
+#define MID_T(k) do { } while (0)
+#endif
+
 template <int NT, int MAXN>
 struct MidSort {
   static constexpr int kWarps = NT / 32;
-  static constexpr int kItems = MAXN / NT;         // keys per thread
+  static constexpr int kItems = MAXN / NT;         // keys (rounds) per thread
+  static constexpr int kRounds = MAXN / 32;        // rounds of 32 keys
   static constexpr int kSlotBits = MAXN == 2048 ? 11 : MAXN == 4096 ? 12 : 13;
-  static constexpr int kDepthBits = 32 - kSlotBits;
-  static constexpr int kDigitBits = 7;
+  static constexpr int kDepthBits = 20;            // quantised depth bits in the key
+  static constexpr int kDigitBits = 4;
   static constexpr int kDigits = 1 << kDigitBits;
-  static constexpr int kCnt = kDigits * kWarps;    // [digit][warp]
+  static constexpr int kCnt = kDigits * kRounds;   // [digit][round]
   static constexpr int kCntPerThread = kCnt / NT;
   static constexpr int kMaxRun = 64;
-  static_assert(MAXN == (1 << kSlotBits), "slot bits");
-  static_assert(kCnt % NT == 0 && (kCntPerThread == 4 || kCntPerThread == 2), "counter layout");
+  static_assert(MAXN == (1 << kSlotBits) && kDepthBits + kSlotBits <= 32, "key layout");
+  static_assert(kCnt % NT == 0 && kCntPerThread % 4 == 0, "counter layout");
   struct Smem {
     unsigned long long s[MAXN];  // full keys, slot order (bitonic fallback: sorted in place)
     uint32_t k32[MAXN];          // scatter buffer, finally the sorted 32-bit keys
@@ -1358,7 +1398,7 @@ struct MidSort {
     uint32_t red[2][kWarps];
   };
 };
-constexpr int kMidThreads = 256;
+constexpr int kMidThreads = 128;
 constexpr int kMidMax = 2048;
 using MidCfg = MidSort<kMidThreads, kMidMax>;
 
@@ -1366,8 +1406,13 @@ using MidCfg = MidSort<kMidThreads, kMidMax>;
 // sorted 32-bit keys (slot = k32 & (MAXN - 1)), false with S.s itself sorted
 // (bitonic fallback).  Block-uniform result.
 template <int NT, int MAXN>
-__device__ __forceinline__ bool block_radix32(typename MidSort<NT, MAXN>::Smem& S, int n) {
+__device__ __forceinline__ bool block_radix32(typename MidSort<NT, MAXN>::Smem& S, int n,
+                                              unsigned long long* prof = nullptr) {
   using M = MidSort<NT, MAXN>;
+#ifdef INPC_PHASE_TIMES
+  long long tp_ = clock64();
+#endif
+  (void)prof;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t lo = 0xFFFFFFFFu, hi = 0u;
@@ -1392,52 +1437,46 @@ __device__ __forceinline__ bool block_radix32(typename MidSort<NT, MAXN>::Smem& 
   const int vbits = range ? 32 - __clz(range) : 0;
   const int shift = vbits > M::kDepthBits ? vbits - M::kDepthBits : 0;
   const int npass = (vbits - shift + M::kDigitBits - 1) / M::kDigitBits;
-  const int E = (n + NT - 1) / NT;          // keys per thread (<= kItems)
-  const int wbase = w * 32 * E;
+  MID_T(2);
+  // warp w owns rounds R = w * E + r (keys 32 R + lane), r < E
+  const int nr = (n + 31) >> 5;
+  const int E = (nr + M::kWarps - 1) / M::kWarps;
   uint32_t kv[M::kItems], rk[M::kItems];
 #pragma unroll
   for (int r = 0; r < M::kItems; ++r) {
-    const int i = wbase + r * 32 + lane;
+    const int i = (w * E + r) * 32 + lane;
     kv[r] = (r < E && i < n) ? ((((uint32_t)(S.s[i] >> 32) - lo) >> shift) << M::kSlotBits) | (uint32_t)i : 0u;
   }
   if (npass == 0) {  // one depth: slot order, fixed below
 #pragma unroll
     for (int r = 0; r < M::kItems; ++r) {
-      const int i = wbase + r * 32 + lane;
+      const int i = (w * E + r) * 32 + lane;
       if (r < E && i < n) S.k32[i] = kv[r];
     }
   }
+  constexpr int Q = M::kCntPerThread / 4;
   for (int p = 0; p < npass; ++p) {
     const int sh = M::kSlotBits + M::kDigitBits * p;
-    if (M::kCntPerThread == 4) reinterpret_cast<uint4*>(S.cnt)[tid] = make_uint4(0u, 0u, 0u, 0u);
-    else reinterpret_cast<uint2*>(S.cnt)[tid] = make_uint2(0u, 0u);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) reinterpret_cast<uint4*>(S.cnt)[tid * Q + q] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < M::kItems; ++r) {
       if (r >= E) break;
-      const int i = wbase + r * 32 + lane;
-      const bool valid = i < n;
-      const uint32_t d = valid ? (kv[r] >> sh) & (uint32_t)(M::kDigits - 1) : (uint32_t)M::kDigits + lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
-      const int leader = __ffs(peers) - 1;
-      uint32_t old = 0u;
-      if (valid && lane == leader) {  // only this warp writes column w; one leader per digit and round
-        old = S.cnt[d * M::kWarps + w];
-        S.cnt[d * M::kWarps + w] = old + (uint32_t)__popc(peers);
-      }
-      old = __shfl_sync(0xffffffffu, old, leader);
-      rk[r] = old + (uint32_t)__popc(peers & lt);
-      __syncwarp();
+      const int R = w * E + r;
+      const bool valid = R * 32 + lane < n;
+      const uint32_t d = (kv[r] >> sh) & (uint32_t)(M::kDigits - 1);
+      const unsigned peers = warp_peers<M::kDigitBits>(d, valid);
+      if (valid && (peers & lt) == 0u) S.cnt[d * M::kRounds + R] = (uint32_t)__popc(peers);
+      rk[r] = (uint32_t)__popc(peers & lt);
     }
     __syncthreads();
-    {  // exclusive scan of the counters in (digit, warp) order
+    {  // exclusive scan of the counters in (digit, round) order
       uint32_t c[M::kCntPerThread], sum = 0u;
-      if (M::kCntPerThread == 4) {
-        const uint4 v = reinterpret_cast<const uint4*>(S.cnt)[tid];
-        c[0] = v.x; c[1] = v.y; c[M::kCntPerThread > 2 ? 2 : 0] = v.z; c[M::kCntPerThread > 3 ? 3 : 0] = v.w;
-      } else {
-        const uint2 v = reinterpret_cast<const uint2*>(S.cnt)[tid];
-        c[0] = v.x; c[1] = v.y;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const uint4 v = reinterpret_cast<const uint4*>(S.cnt)[tid * Q + q];
+        c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
       }
 #pragma unroll
       for (int q = 0; q < M::kCntPerThread; ++q) sum += c[q];
@@ -1450,36 +1489,37 @@ __device__ __forceinline__ bool block_radix32(typename MidSort<NT, MAXN>::Smem& 
       if (lane == 31) S.wsum[w] = x;
       __syncthreads();
       uint32_t run = x - sum;
-      for (int q = 0; q < w; ++q) run += S.wsum[q];
+#pragma unroll
+      for (int q = 0; q < M::kWarps; ++q) run += q < w ? S.wsum[q] : 0u;
 #pragma unroll
       for (int q = 0; q < M::kCntPerThread; ++q) {
         const uint32_t cq = c[q];
         c[q] = run;
         run += cq;
       }
-      if (M::kCntPerThread == 4)
-        reinterpret_cast<uint4*>(S.cnt)[tid] = make_uint4(c[0], c[1], c[M::kCntPerThread > 2 ? 2 : 0],
-                                                         c[M::kCntPerThread > 3 ? 3 : 0]);
-      else
-        reinterpret_cast<uint2*>(S.cnt)[tid] = make_uint2(c[0], c[1]);
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        reinterpret_cast<uint4*>(S.cnt)[tid * Q + q] = make_uint4(c[4 * q], c[4 * q + 1], c[4 * q + 2], c[4 * q + 3]);
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < M::kItems; ++r) {
       if (r >= E) break;
-      const int i = wbase + r * 32 + lane;
-      if (i < n) S.k32[S.cnt[((kv[r] >> sh) & (uint32_t)(M::kDigits - 1)) * M::kWarps + w] + rk[r]] = kv[r];
+      const int R = w * E + r;
+      if (R * 32 + lane < n)
+        S.k32[S.cnt[((kv[r] >> sh) & (uint32_t)(M::kDigits - 1)) * M::kRounds + R] + rk[r]] = kv[r];
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < M::kItems; ++r) {
       if (r >= E) break;
-      const int i = wbase + r * 32 + lane;
+      const int i = (w * E + r) * 32 + lane;
       if (i < n) kv[r] = S.k32[i];
     }
   }
   __syncthreads();
-  // runs of equal truncated depth: (depth, index) order on the full keys
+  MID_T(3);
+  // runs of equal quantised depth: (depth, index) order on the full keys
   constexpr uint32_t smask = (uint32_t)MAXN - 1u;
   bool bad = false;
   for (int p = tid; p + 1 < n; p += NT) {
@@ -1508,228 +1548,73 @@ __device__ __forceinline__ bool block_radix32(typename MidSort<NT, MAXN>::Smem& 
     for (int k = n + tid; k < np; k += NT) S.s[k] = ~0ull;
     __syncthreads();
     block_bitonic_fast(S.s, np);
+    MID_T(4);
     return false;
   }
+  MID_T(4);
   return true;
 }
 
-// Warp-level variant for tiles of up to kWarpMidMax entries (the bulk of the
-// mid tiles): one warp sorts one tile alone -- 256 per-warp digit counters
-// (8-bit digits, 10 slot bits, 22 depth bits: three passes), no block
-// barriers, the warp's keys and ranks in registers.
-constexpr int kWarpMidMax = 1024;
-struct WarpMidSmem {
-  unsigned long long s[kWarpMidMax];
-  uint32_t k32[kWarpMidMax];
-  __align__(16) uint32_t cnt[256];
-};
-
-// 64-bit bitonic sort of np (power of two) keys in SMEM by one warp
-// (fallback for long runs of equal depth).
-__device__ __forceinline__ void warp_bitonic_smem(unsigned long long* s, int np, int lane) {
-  for (int k = 2; k <= np; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = lane; t < (np >> 1); t += 32) {
-        const int i = 2 * t - (t & (j - 1));
-        const int ixj = i + j;
-        const unsigned long long a = s[i], b = s[ixj];
-        if ((a > b) == ((i & k) == 0)) {
-          s[i] = b;
-          s[ixj] = a;
-        }
-      }
-      __syncwarp();
-    }
-}
-
-// Sort the n <= kWarpMidMax keys of W.s (slot order) into sorted_idx[0..n).
-__device__ __forceinline__ void warp_radix32_tile(WarpMidSmem& W, int n, uint32_t* __restrict__ out, int lane,
-                                                  int kDepth) {
-  constexpr int kSlot = 10, kDig = 8, kE = kWarpMidMax / 32;
-  const uint32_t lt = (1u << lane) - 1u;
-  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
-  for (int k = lane; k < n; k += 32) {
-    const uint32_t d = (uint32_t)(W.s[k] >> 32);
-    lo = min(lo, d);
-    hi = max(hi, d);
-  }
-  lo = __reduce_min_sync(0xffffffffu, lo);
-  hi = __reduce_max_sync(0xffffffffu, hi);
-  const uint32_t range = hi - lo;
-  const int vbits = range ? 32 - __clz(range) : 0;
-  const int shift = vbits > kDepth ? vbits - kDepth : 0;
-  const int npass = (vbits - shift + kDig - 1) / kDig;
-  const int E = (n + 31) >> 5;
-  uint32_t kv[kE], rk[kE];
-#pragma unroll
-  for (int r = 0; r < kE; ++r) {
-    const int i = r * 32 + lane;
-    kv[r] = (r < E && i < n) ? ((((uint32_t)(W.s[i] >> 32) - lo) >> shift) << kSlot) | (uint32_t)i : 0u;
-    if (npass == 0 && r < E && i < n) W.k32[i] = kv[r];
-  }
-  for (int p = 0; p < npass; ++p) {
-    const int sh = kSlot + kDig * p;
-    reinterpret_cast<uint4*>(W.cnt)[2 * lane] = make_uint4(0u, 0u, 0u, 0u);
-    reinterpret_cast<uint4*>(W.cnt)[2 * lane + 1] = make_uint4(0u, 0u, 0u, 0u);
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < kE; ++r) {
-      if (r >= E) break;
-      const bool valid = r * 32 + lane < n;
-      const uint32_t d = valid ? (kv[r] >> sh) & 255u : 256u + lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
-      const int leader = __ffs(peers) - 1;
-      uint32_t old = 0u;
-      if (valid && lane == leader) {
-        old = W.cnt[d];
-        W.cnt[d] = old + (uint32_t)__popc(peers);
-      }
-      rk[r] = __shfl_sync(0xffffffffu, old, leader) + (uint32_t)__popc(peers & lt);
-      __syncwarp();
-    }
-    {  // exclusive scan of the 256 counters: lane owns [8 lane, 8 lane + 8)
-      const uint4 a = reinterpret_cast<const uint4*>(W.cnt)[2 * lane];
-      const uint4 b = reinterpret_cast<const uint4*>(W.cnt)[2 * lane + 1];
-      const uint32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      uint32_t sum = 0u;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) sum += c[q];
-      uint32_t x = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      uint32_t e[8], run = x - sum;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        e[q] = run;
-        run += c[q];
-      }
-      __syncwarp();
-      reinterpret_cast<uint4*>(W.cnt)[2 * lane] = make_uint4(e[0], e[1], e[2], e[3]);
-      reinterpret_cast<uint4*>(W.cnt)[2 * lane + 1] = make_uint4(e[4], e[5], e[6], e[7]);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < kE; ++r) {
-      if (r >= E) break;
-      if (r * 32 + lane < n) W.k32[W.cnt[(kv[r] >> sh) & 255u] + rk[r]] = kv[r];
-    }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < kE; ++r) {
-      if (r >= E) break;
-      if (r * 32 + lane < n) kv[r] = W.k32[r * 32 + lane];
-    }
-    __syncwarp();
-  }
-  __syncwarp();
-  constexpr uint32_t smask = (uint32_t)kWarpMidMax - 1u;
-  bool bad = false;
-  for (int p = lane; p + 1 < n; p += 32) {  // runs of equal truncated depth: full-key order
-    const uint32_t a = W.k32[p] >> kSlot;
-    if ((W.k32[p + 1] >> kSlot) != a || (p > 0 && (W.k32[p - 1] >> kSlot) == a)) continue;
-    int end = p + 2;
-    while (end < n && (W.k32[end] >> kSlot) == a && end - p <= MidCfg::kMaxRun) ++end;
-    if (end - p > MidCfg::kMaxRun) {
-      bad = true;
-      continue;
-    }
-    for (int k = p + 1; k < end; ++k) {
-      const uint32_t v = W.k32[k];
-      const unsigned long long fv = W.s[v & smask];
-      int j = k - 1;
-      while (j >= p && W.s[W.k32[j] & smask] > fv) {
-        W.k32[j + 1] = W.k32[j];
-        --j;
-      }
-      W.k32[j + 1] = v;
-    }
-  }
-  if (__any_sync(0xffffffffu, bad)) {
-    int np = 64;
-    while (np < n) np <<= 1;
-    for (int k = n + lane; k < np; k += 32) W.s[k] = ~0ull;
-    __syncwarp();
-    warp_bitonic_smem(W.s, np, lane);
-    for (int k = lane; k < n; k += 32) out[k] = (uint32_t)W.s[k];
-  } else {
-    __syncwarp();
-    for (int k = lane; k < n; k += 32) out[k] = (uint32_t)W.s[W.k32[k] & smask];
-  }
-  __syncwarp();
-}
-
-// Mid tiles of the big-tile list (kWarpSortCap < n <= kMidMax; larger tiles
-// are left to k_sort_big): first every warp takes tiles of up to
-// kWarpMidMax entries alone (warp-stride over the list), then the CTA sorts
-// the tiles of kWarpMidMax + 1 .. kMidMax entries together (block_radix32).
-constexpr int kSortMidWarps = kMidThreads / 32;
-constexpr size_t kSortMidSmem =
-    sizeof(WarpMidSmem) * kSortMidWarps > sizeof(MidCfg::Smem) ? sizeof(WarpMidSmem) * kSortMidWarps
-                                                                : sizeof(MidCfg::Smem);
+// The mid tiles (kWarpSortCap < n <= kMidMax; larger ones are left to
+// k_sort_big), one CTA per tile (block_radix32), grid-stride over the
+// big-tile list.  Its last CTA zeroes the list count for the next call.
+// (A one-warp-per-tile variant with the same ranking measured 16.6 vs
+// 13.4 ms per cfg 5 step: fewer tiles in flight did not pay for the
+// barriers saved.)
 __global__ void __launch_bounds__(kMidThreads) k_sort_mid(const uint32_t* __restrict__ ranges,
-                                                          const uint32_t* __restrict__ big_tiles,
-                                                          const ViewScalars* __restrict__ sc,
-                                                          const unsigned long long* __restrict__ entries,
-                                                          uint32_t* __restrict__ sorted_idx,
-                                                          uint32_t warp_max, int qbits,
-                                                          uint32_t* __restrict__ dispenser) {
-  extern __shared__ __align__(16) unsigned char mid_smem[];
+                                                              const uint32_t* __restrict__ big_tiles,
+                                                              ViewScalars* __restrict__ sc,
+                                                              const unsigned long long* __restrict__ entries,
+                                                              uint32_t* __restrict__ sorted_idx,
+                                                              uint32_t* __restrict__ done) {
+  __shared__ MidCfg::Smem S;
+  __shared__ uint32_t s_last;
   const uint32_t nb = sc->num_big;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  {
-    WarpMidSmem& W = reinterpret_cast<WarpMidSmem*>(mid_smem)[warp];
-    // tiles handed out one per warp by an atomic dispenser (sizes vary)
-    uint32_t j = 0;
-    if (lane == 0) j = atomicAdd(dispenser, 1u);
-    j = __shfl_sync(0xffffffffu, j, 0);
-    while (j < nb) {
-      const uint32_t t = big_tiles[j];
-      const uint32_t begin = ranges[t], n = ranges[t + 1] - begin;
-      uint32_t jn = 0;
-      if (lane == 0) jn = atomicAdd(dispenser, 1u);
-      if (n <= warp_max) {  // warp-uniform
-        for (int k = lane; k < (int)n; k += 32) cp_async8(&W.s[k], entries + begin + k);
-        cp_async_wait_all8();
-        __syncwarp();
-        warp_radix32_tile(W, (int)n, sorted_idx + begin, lane, qbits);
-      }
-      j = __shfl_sync(0xffffffffu, jn, 0);
-    }
-  }
-  __syncthreads();
-  MidCfg::Smem& S = *reinterpret_cast<MidCfg::Smem*>(mid_smem);
+#ifdef INPC_PHASE_TIMES
+  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tp_ = clock64();
+#else
+  unsigned long long* prof = nullptr;
+#endif
   for (uint32_t j = blockIdx.x; j < nb; j += gridDim.x) {
     const uint32_t t = big_tiles[j];
     const uint32_t begin = ranges[t], n = ranges[t + 1] - begin;
-    if (n <= warp_max || n > (uint32_t)kMidMax) continue;  // block-uniform
+    if (n > (uint32_t)kMidMax) continue;  // block-uniform
+    MID_T(0);
     for (int k = threadIdx.x; k < (int)n; k += kMidThreads) cp_async8(&S.s[k], entries + begin + k);
     cp_async_wait_all8();
     __syncthreads();
-    if (block_radix32<kMidThreads, kMidMax>(S, (int)n)) {
+    MID_T(1);
+#ifdef INPC_PHASE_TIMES
+    const bool ok = block_radix32<kMidThreads, kMidMax>(S, (int)n, prof);
+    tp_ = clock64();
+#else
+    const bool ok = block_radix32<kMidThreads, kMidMax>(S, (int)n);
+#endif
+    if (ok) {
       for (int k = threadIdx.x; k < (int)n; k += kMidThreads)
         sorted_idx[begin + k] = (uint32_t)S.s[S.k32[k] & (uint32_t)(kMidMax - 1)];
     } else {
       for (int k = threadIdx.x; k < (int)n; k += kMidThreads) sorted_idx[begin + k] = (uint32_t)S.s[k];
     }
     __syncthreads();
+    MID_T(5);
+    if (prof && threadIdx.x == 0) prof[6] += 1;
   }
-  // the last CTA to finish zeroes the dispenser for the next call
-  __shared__ uint32_t s_last;
+#ifdef INPC_PHASE_TIMES
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 7; ++k) atomicAdd(&g_mid_cyc[k], prof[k]);
+#endif
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    s_last = atomicAdd(dispenser + 1, 1u) == gridDim.x - 1;
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {  // every CTA has read the big-tile list count
-    dispenser[0] = 0u;
-    dispenser[1] = 0u;
-    ViewScalars* scw = const_cast<ViewScalars*>(sc);
-    scw->num_big = 0u;
-    scw->max_big = 0u;
+  if (s_last && threadIdx.x == 0) {  // every CTA has read the list count
+    *done = 0u;
+    sc->num_big = 0u;
+    sc->max_big = 0u;
   }
 }
 

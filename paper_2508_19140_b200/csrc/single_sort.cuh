@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_rx_hist(const unsigned long l
 }
 
 // Stable scatter: rounds of 32 consecutive elements in order; lanes with the
-// same digit rank themselves with __match_any_sync; the warp's running
+// same digit rank themselves (warp_peers ballots); the warp's running
 // per-digit cursor starts at the scanned offset of (digit, tile).
 __global__ void __launch_bounds__(kRxWarps * 32) k_rx_scatter(
     const unsigned long long* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t n, int shift,
@@ -85,13 +85,13 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_rx_scatter(
     const int64_t e = base + r * 32 + lane;
     const bool valid = e < n;
     unsigned long long k = 0;
-    uint32_t v = 0, d = 256u + lane;  // invalid lanes match nobody
+    uint32_t v = 0, d = 0u;
     if (valid) {
       k = kin[e];
       v = vin[e];
       d = (uint32_t)(k >> shift) & 255u;
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned peers = warp_peers<8>(d, valid);
     if (valid) {
       const uint32_t pos = cur[warp][d] + __popc(peers & lt);
       kout[pos] = k;

@@ -218,9 +218,22 @@ def test_invalid_args(inpc, ctx):
         ctx.forward(cfg, c["cams"], xyz, feat, op)
     assert e.value.status == inpc.INVALID_ARG
     cfg = inpc.make_cfg(64, 64, 4)
-    with pytest.raises(inpc.RasterError) as e:   # host pointer
+    with pytest.raises(inpc.RasterError) as e:   # host tensor (binding check)
         ctx.forward(cfg, c["cams"], torch.from_numpy(c["xyz"]), feat, op)
     assert e.value.status == inpc.INVALID_ARG
+    with pytest.raises(inpc.RasterError) as e:   # wrong dtype (binding check)
+        ctx.forward(cfg, c["cams"], xyz, feat.double(), op)
+    assert e.value.status == inpc.INVALID_ARG
+    # the library's own check of a host pointer, through the raw C ABI
+    import ctypes as ct
+    xh = torch.from_numpy(c["xyz"])
+    out = torch.empty((1, 64, 64, 4), device="cuda")
+    cams, V = inpc._cams(c["cams"])
+    st = inpc.lib.inpc_rasterize_fwd(ctx._h, ct.byref(cfg), cams, V, ct.c_void_p(xh.data_ptr()),
+                                     ct.c_void_p(feat.data_ptr()), 0, ct.c_void_p(op.data_ptr()),
+                                     xh.shape[0], None, 0, ct.c_void_p(out.data_ptr()), None, None,
+                                     None, None, inpc._stream(None))
+    assert st == inpc.INVALID_ARG
     fresh = inpc.Context(0)
     with pytest.raises(inpc.RasterError) as e:
         fresh.backward(cfg, c["cams"], xyz, feat, op, torch.zeros((1, 64, 64, 4), device="cuda"))

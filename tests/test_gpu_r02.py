@@ -222,3 +222,55 @@ def test_cfg4_spatial_order_sampled(inpc, ctx):
         ty, tx = divmod(int(t), 240)
         mask[ty * 8:(ty + 1) * 8, tx * 8:(tx + 1) * 8] = True
     check_image(c, res, "bilinear", pixel_mask=mask)
+
+
+def test_two_graphs_in_flight_and_shared_context_guard(inpc):
+    """two rasterize() calls before their backwards each keep
+    their own saved state (pooled contexts); with one explicit shared
+    context the stale backward raises instead of using the newer state."""
+    c = synthgen.config1(seed=21)
+    H, W, C = c["H"], c["W"], c["C"]
+    xyz = dev(c["xyz"])
+    cams2 = [synthgen.camera(np.eye(3), [0.05, 0.0, 0.1], 64, 64, 32, 32, 0.1)]
+    gF, gA, gD = (dev(x) for x in synthgen.upstream_grads(2, 1, H, W, C))
+
+    def grads(cams, ctx_arg=None):
+        f = dev(c["feat"]).requires_grad_(True)
+        o = dev(c["opacity"]).requires_grad_(True)
+        F, A, D = inpc.rasterize(xyz, f, o, cams, H, W, context=ctx_arg)
+        return f, o, (F * gF).sum() + (A * gA).sum() + (D * gD).sum()
+
+    f1, o1, l1 = grads(c["cams"])
+    f2, o2, l2 = grads(cams2)          # second forward before the first backward
+    l1.backward()
+    l2.backward()
+    for cams, f, o in ((c["cams"], f1, o1), (cams2, f2, o2)):
+        g = oracle.backward(cams[0], c["xyz"], c["feat"], c["opacity"], H, W, *(x[0].cpu().numpy() for x in (gF, gA, gD)))
+        check_grads(f.grad.cpu().numpy(), g["g_feat"])
+        check_grads(o.grad.cpu().numpy(), g["g_opacity"])
+    shared = inpc.Context(0)
+    _, _, m1 = grads(c["cams"], shared)
+    _, _, m2 = grads(cams2, shared)
+    with pytest.raises(RuntimeError, match="overwritten"):
+        m1.backward()
+    m2.backward()
+    shared.close()
+
+
+def test_rasterize_sh_and_env_arguments(inpc):
+    """rasterize() takes C from [N, C, 9] with FLAG_SH_FEATURES and
+    passes env_hw for an environment-map background."""
+    c, sh = synthgen.config1(seed=23), None
+    sh = np.random.default_rng(3).normal(0, 0.5, (c["xyz"].shape[0], 4, 9)).astype(np.float32)
+    F, A, D = inpc.rasterize(dev(c["xyz"]), dev(sh), dev(c["opacity"]), c["cams"], 64, 64,
+                             flags=inpc.FLAG_SH_FEATURES)
+    assert F.shape == (1, 64, 64, 4)
+    f_or, _ = oracle.sh_features(c["cams"][0], c["xyz"], sh)
+    r = oracle.render(c["cams"][0], c["xyz"], f_or, c["opacity"], 64, 64)
+    np.testing.assert_allclose(F[0].cpu().numpy(), r["F"], atol=IMG_TOL)
+    env = np.random.default_rng(4).uniform(-1, 1, (16, 32, 4)).astype(np.float32)
+    F2, _, _ = inpc.rasterize(dev(c["xyz"]), dev(c["feat"]), dev(c["opacity"]), c["cams"], 64, 64,
+                              bg=dev(env), env_hw=env.shape[:2])
+    bg = oracle.env_background(c["cams"][0], env, 64, 64)
+    r2 = oracle.render(c["cams"][0], c["xyz"], c["feat"], c["opacity"], 64, 64, bg=bg)
+    np.testing.assert_allclose(F2[0].cpu().numpy(), r2["F"], atol=IMG_TOL)
