@@ -296,9 +296,10 @@ class Context:
         _check_tensor("feat", feat, dev, _feat_shape(cfg, N, feat))
         _check_tensor("opacity", opacity, dev, (N,))
         _check_tensor("bg", bg, dev, allow_none=True)
-        _check_tensor("gF", gF, dev, (V, H, W, C))
-        _check_tensor("gA", gA, dev, (V, H, W), allow_none=True)
-        _check_tensor("gD", gD, dev, (V, H, W), allow_none=True)
+        lead = (V,) if gF.dim() == 4 or V > 1 else ()   # one view: [H,W,C] / [H,W] also accepted
+        _check_tensor("gF", gF, dev, lead + (H, W, C))
+        _check_tensor("gA", gA, dev, lead + (H, W), allow_none=True)
+        _check_tensor("gD", gD, dev, lead + (H, W), allow_none=True)
         fstride, bstride = _strides(cfg, N, feat, bg)
         if g_feat is None:
             g_feat = torch.zeros_like(feat)
