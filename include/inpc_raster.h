@@ -23,8 +23,13 @@
  *     HOST structs, read during the call only.
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  All GPU
  *     work is enqueued on it, asynchronously; argument errors are reported
- *     synchronously before anything is enqueued.  Gaussian-mode forward
- *     synchronises the stream once to size its fragment buffer.
+ *     synchronously before anything is enqueued.  The Gaussian-mode forward
+ *     sizes its fragment buffers from a static bound of the entries per
+ *     point (3-sigma radius bound from sigma, dilation, z_near and the
+ *     intrinsics) when that fits a quarter of the free device memory, and
+ *     is then free of host synchronisation (graph-capturable); otherwise
+ *     (huge world sigma) it synchronises the stream once per view to read
+ *     the entry count back.
  *   - Ownership: inputs/outputs are caller-owned and borrowed for the
  *     stream-ordered duration of the call.  The ctx owns its scratch arena
  *     and the state the forward saves for the backward (per-tile lists,

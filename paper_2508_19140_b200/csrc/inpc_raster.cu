@@ -289,6 +289,41 @@ void make_dev(const inpc_raster_cfg* cfg, const inpc_camera& cam, DevCam& dc, De
   g.env_w = cfg->env_w;
 }
 
+// Upper bound of the tiles one Gaussian footprint can touch in a view (R15-
+// R17), or 0 when none can be given (the caller then reads F_t back).
+// The 3-sigma radius satisfies r^2 <= 9 (a + c) (lambda_max <= trace) with
+// a = s^2 jx^2 (1 + xz^2) + dil, s jx <= s fx / z_near = px (z > z_near), and
+// a footprint that meets the image has |fx xz| <= mx + r (mx = the larger
+// distance of cx to the image edges), so r^2 <= A + B r + K r^2 with
+//   A = 9 (px^2 (1 + mx^2/fx^2) + py^2 (1 + my^2/fy^2) + 2 dil),
+//   B = 18 (px^2 mx / fx^2 + py^2 my / fy^2),  K = 9 (px^2/fx^2 + py^2/fy^2),
+// finite when K < 1 (s well below z_near / 3: the paper's auto sigma gives
+// K ~ 1e-4).  SIGMA_IS_PIXELS: r = 3 sqrt(sigma^2 + dil) exactly.  A span of
+// 2r pixels covers at most floor(2r / 8) + 2 tile columns.
+uint64_t gauss_tiles_bound(const inpc_raster_cfg* cfg, const inpc_camera& cam, int band_rows, int tiles_x) {
+  double r;
+  const double dil = cfg->dilation;
+  if (cfg->flags & INPC_FLAG_SIGMA_IS_PIXELS) {
+    r = 3.0 * sqrt((double)cfg->sigma * cfg->sigma + dil);
+  } else {
+    const double fx = cam.fx, fy = cam.fy;
+    const double sg = cfg->sigma > 0.0f ? (double)cfg->sigma : 5.0 * cam.z_near / (fx > fy ? fx : fy);
+    const double px = sg * fx / cam.z_near, py = sg * fy / cam.z_near;
+    const double mx = fmax(fabs((double)cam.cx), fabs((double)cfg->W - cam.cx));
+    const double my = fmax(fabs((double)cam.cy), fabs((double)cfg->H - cam.cy));
+    const double K = 9.0 * (px * px / (fx * fx) + py * py / (fy * fy));
+    if (!(K < 0.5)) return 0;
+    const double A = 9.0 * (px * px * (1.0 + mx * mx / (fx * fx)) + py * py * (1.0 + my * my / (fy * fy)) + 2.0 * dil);
+    const double B = 18.0 * (px * px * mx / (fx * fx) + py * py * my / (fy * fy));
+    r = (B + sqrt(B * B + 4.0 * (1.0 - K) * A)) / (2.0 * (1.0 - K));
+  }
+  if (!isfinite(r)) return 0;
+  r = r * 1.01 + 1.0;  // fp32 rounding of the kernel's covariance, conic and radius
+  const double span = floor(2.0 * r / kTile) + 2.0;
+  const uint64_t tx = (uint64_t)fmin(span, (double)tiles_x), ty = (uint64_t)fmin(span, (double)band_rows);
+  return tx * ty;
+}
+
 int cmax_for(int C) { return C <= 4 ? 4 : C <= 8 ? 8 : C <= 16 ? 16 : C <= 32 ? 32 : 64; }
 
 template <typename K>
@@ -749,11 +784,26 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     }
     uint64_t need = bound;
     if (gauss) {
-      // the one data-dependent size: read F_t back (Gaussian footprints are unbounded)
-      CK(cudaMemcpyAsync(c->host_scalars, sc, sizeof(ViewScalars), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      need = c->host_scalars[0];
-      if (need >= 0xFFFFFFFFull) return INPC_KEY_OVERFLOW;
+      // the one data-dependent size.  Sync-free (graph-capturable) when a
+      // static bound of the entry count fits the memory budget (a quarter of
+      // the free device memory): the buffers are sized for the bound;
+      // otherwise F_t is read back once per view
+      const uint64_t per_pt = gauss_tiles_bound(cfg, cams[v], g.ty1 - g.ty0, g.tiles_x);
+      const uint64_t ub = per_pt * (uint64_t)N;
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        free_b = 0;
+      }
+      const bool have = vs.idx_cap >= ub;  // already sized for the bound
+      if (per_pt && ub < 0xFFFFFFFFull && (have || ub * 20ull <= (uint64_t)(free_b / 4))) {
+        need = ub;
+      } else {
+        CK(cudaMemcpyAsync(c->host_scalars, sc, sizeof(ViewScalars), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        need = c->host_scalars[0];
+        if (need >= 0xFFFFFFFFull) return INPC_KEY_OVERFLOW;
+      }
     }
     if (!fused_kp) {
       if ((st = ensure(c->entries, (size_t)(need ? need : 1) * 8, s))) return st;
