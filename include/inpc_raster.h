@@ -208,6 +208,22 @@ INPC_API int inpc_sort_single64(inpc_ctx* ctx, const inpc_raster_cfg* cfg, const
  * Asynchronous on stream. */
 INPC_API int inpc_spatial_order(inpc_ctx* ctx, const float* xyz, int64_t N, uint32_t* perm, void* stream);
 
+/* Chunk bounds of a static cloud: box
+ * [ceil(N / 1024), 6] (device, fp32) receives, for every chunk of 1024
+ * consecutive points, (xmin, ymin, zmin, xmax, ymax, zmax) over its finite
+ * points (min > max when it has none).  Meant for a spatially ordered cloud
+ * (inpc_spatial_order), where the chunks are compact.  Asynchronous. */
+INPC_API int inpc_chunk_bounds(inpc_ctx* ctx, const float* xyz, int64_t N, float* box, void* stream);
+/* Attach chunk bounds to the context (box NULL detaches).  Forwards whose
+ * xyz pointer and N equal the ones given here then skip, in the bilinear
+ * binning of large clouds, every chunk whose box cannot produce a footprint
+ * in the view's frame or screen band (behind the near plane, or projecting
+ * wholly outside the image / band): a conservative test, the rasterized
+ * result is unchanged.  The caller keeps box alive and in step with the
+ * cloud's contents.  Not used with INPC_FLAG_DEBUG (its per-point exports
+ * cover every point). */
+INPC_API int inpc_ctx_set_chunks(inpc_ctx* ctx, const float* xyz, int64_t N, const float* box);
+
 /* Per-stage device timing (CUDA events around each stage; adds no sync to
  * the calls).  inpc_ctx_stage_times waits for the recorded events, adds
  * their elapsed milliseconds to per-stage accumulators and returns the

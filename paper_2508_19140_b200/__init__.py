@@ -33,7 +33,8 @@ TILE = 8
 EXPORTS = ("inpc_ctx_create", "inpc_ctx_destroy", "inpc_rasterize_fwd", "inpc_rasterize_bwd",
            "inpc_debug_export", "inpc_ctx_set_profiling", "inpc_ctx_stage_times",
            "inpc_ctx_forget_events", "inpc_ctx_set_allocator", "inpc_sort_single64",
-           "inpc_stage_name", "inpc_status_string", "inpc_version", "inpc_spatial_order")
+           "inpc_stage_name", "inpc_status_string", "inpc_version", "inpc_spatial_order",
+           "inpc_chunk_bounds", "inpc_ctx_set_chunks")
 
 
 # inpc_alloc_fn / inpc_free_fn (include/inpc_raster.h)
@@ -95,6 +96,8 @@ def _load():
     lib.inpc_sort_single64.argtypes = [P, P, P, P, P, i64, P, P, i64, ct.POINTER(i64), P]
     lib.inpc_ctx_set_allocator.argtypes = [P, ALLOC_FN, FREE_FN, P]
     lib.inpc_spatial_order.argtypes = [P, P, i64, P, P]
+    lib.inpc_chunk_bounds.argtypes = [P, P, i64, P, P]
+    lib.inpc_ctx_set_chunks.argtypes = [P, P, i64, P]
     lib.inpc_stage_name.argtypes = [i32]
     lib.inpc_stage_name.restype = ct.c_char_p
     lib.inpc_status_string.argtypes = [ct.c_int]
@@ -362,6 +365,22 @@ class Context:
         perm = torch.empty(max(N, 1), dtype=torch.int32, device=xyz.device)
         _check(lib.inpc_spatial_order(self._h, _ptr(xyz), N, _ptr(perm), _stream(stream)))
         return perm[:N].long()
+
+    def set_chunks(self, xyz, stream=None):
+        """Compute the chunk bounds of the static cloud `xyz` (inpc_chunk_bounds)
+        and attach them: forwards over this same tensor then skip chunks that
+        cannot reach the frame / screen band.  set_chunks(None) detaches."""
+        import torch
+        if xyz is None:
+            _check(lib.inpc_ctx_set_chunks(self._h, None, 0, None))
+            self._chunk_box = None
+            return None
+        N = xyz.shape[0]
+        box = torch.empty(((N + 1023) // 1024, 6), dtype=torch.float32, device=xyz.device)
+        _check(lib.inpc_chunk_bounds(self._h, _ptr(xyz), N, _ptr(box), _stream(stream)))
+        _check(lib.inpc_ctx_set_chunks(self._h, _ptr(xyz), N, _ptr(box)))
+        self._chunk_box = (xyz, box)      # both kept alive with the context
+        return box
 
     def set_profiling(self, on=True):
         _check(lib.inpc_ctx_set_profiling(self._h, 1 if on else 0))

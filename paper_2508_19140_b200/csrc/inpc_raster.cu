@@ -74,6 +74,11 @@ struct inpc_ctx {
   int big_grid = 0;
   int mid_grid = 0;       // k_sort_mid: resident CTAs (grid-stride over the big-tile list)
   bool no_mid_sort = false; // env INPC_NO_MID_SORT=1: every big tile through k_sort_big (A/B)
+  // chunk bounds of a static cloud (inpc_ctx_set_chunks): used by forwards over that cloud
+  const float* chunk_box = nullptr;
+  const float* chunk_xyz = nullptr;
+  int64_t chunk_N = 0;
+  Buf chunk_alive;
   // scratch (shared by views, stream ordered)
   Buf scat;  // unfused bilinear binning: depth key + tile block | corner mask per point
   Buf zeroed, cursor, big_tiles, huge_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg, g_eval;
@@ -173,7 +178,7 @@ struct AllocScope {
 };
 
 void release_all(inpc_ctx* c) {
-  for (Buf* b : {&c->scat, &c->zeroed, &c->cursor, &c->big_tiles, &c->huge_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots,
+  for (Buf* b : {&c->chunk_alive, &c->scat, &c->zeroed, &c->cursor, &c->big_tiles, &c->huge_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots,
                  &c->agg, &c->g_eval, &c->tmp, &c->overflow, &c->f4_rec, &c->f4_keys, &c->f4_vals,
                  &c->f4_keys2, &c->f4_vals2, &c->f4_hist, &c->f4_scan, &c->f4_misc})
     free_buf(*b);
@@ -755,22 +760,33 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       if ((st = ensure(c->scat, (size_t)N * 8, s))) return st;
       scp = (uint2*)c->scat.p;
     }
+    // chunk culling: bilinear unfused path over the cloud the bounds describe (not in
+    // debug mode, whose per-point exports cover every point)
+    const float* cbox = (scp && !gauss && !debug && c->chunk_box && c->chunk_xyz == xyz && c->chunk_N == N)
+                            ? c->chunk_box : nullptr;
+    uint8_t* calive = nullptr;
+    if (cbox) {
+      if ((st = ensure(c->chunk_alive, (size_t)nblk, s))) return st;
+      calive = (uint8_t*)c->chunk_alive.p;
+    }
     if (N > 0 && !fused_kp) {
       StageTimer tm(c, s, kStProject, 1);
       PointRec* recp = (PointRec*)vs.rec.p;
       uint4* slp = (uint4*)c->slots.p;
       if (gauss && sh)
         k_project_count<1, true><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N, recp,
-                                                                 tc, nullptr, dk, dt, feat_out, nullptr);
+                                                                 tc, nullptr, dk, dt, feat_out, nullptr,
+                                                                 nullptr, nullptr);
       else if (gauss)
         k_project_count<1, false><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N, recp,
-                                                                  tc, nullptr, dk, dt, feat_out, nullptr);
+                                                                  tc, nullptr, dk, dt, feat_out, nullptr,
+                                                                  nullptr, nullptr);
       else if (sh)
         k_project_count<0, true><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N, recp,
-                                                                 tc, slp, dk, dt, feat_out, scp);
+                                                                 tc, slp, dk, dt, feat_out, scp, cbox, calive);
       else
         k_project_count<0, false><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N, recp,
-                                                                  tc, slp, dk, dt, feat_out, scp);
+                                                                  tc, slp, dk, dt, feat_out, scp, cbox, calive);
       CK(cudaGetLastError());
     }
     if (!fused_kp) {
@@ -821,7 +837,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
         k_scatter_slots<<<nblk, kPointThreads, 0, s>>>(g, (const PointRec*)vs.rec.p,
                                                        (const uint4*)c->slots.p, N,
                                                        (const uint32_t*)vs.ranges.p,
-                                                       (unsigned long long*)c->entries.p, scp);
+                                                       (unsigned long long*)c->entries.p, scp, calive);
       CK(cudaGetLastError());
     }
     if (N > kWarpSortCap && !fused_kp && !c->no_mid_sort) {  // tiles of 257..kMidMax entries
@@ -1053,7 +1069,7 @@ int inpc_sort_single64(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     const int nblk = (int)((N + (int64_t)kPointThreads * kPPT - 1) / ((int64_t)kPointThreads * kPPT));
     k_project_count<0, false><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, nullptr, false, N,
                                                               (PointRec*)c->f4_rec.p, nullptr, nullptr,
-                                                              nullptr, nullptr, nullptr, nullptr);
+                                                              nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
     CK(cudaGetLastError());
   }
   unsigned long long* ka = (unsigned long long*)c->f4_keys.p;
@@ -1095,6 +1111,29 @@ int inpc_sort_single64(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   if (F_out) *F_out = F;
   if (sorted_idx && F > 0)
     CK(cudaMemcpyAsync(sorted_idx, va, (size_t)(F < sorted_cap ? F : sorted_cap) * 4, cudaMemcpyDeviceToDevice, s));
+  return INPC_OK;
+}
+
+int inpc_chunk_bounds(inpc_ctx* c, const float* xyz, int64_t N, float* box, void* stream) {
+  if (!c || N < 0) return INPC_INVALID_ARG;
+  if (N == 0) return INPC_OK;
+  DeviceGuard dg(c->device);
+  if (!is_device_ptr(xyz) || !is_device_ptr(box)) return INPC_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaGetLastError();
+  const int64_t nchunks = (N + kChunkPoints - 1) / kChunkPoints;
+  k_chunk_bounds<<<(unsigned)nchunks, kPointThreads, 0, s>>>(xyz, N, box);
+  CK(cudaGetLastError());
+  return INPC_OK;
+}
+
+int inpc_ctx_set_chunks(inpc_ctx* c, const float* xyz, int64_t N, const float* box) {
+  if (!c || N < 0) return INPC_INVALID_ARG;
+  DeviceGuard dg(c->device);
+  if (box && (!is_device_ptr(box) || !is_device_ptr(xyz))) return INPC_INVALID_ARG;
+  c->chunk_box = box;
+  c->chunk_xyz = box ? xyz : nullptr;
+  c->chunk_N = box ? N : 0;
   return INPC_OK;
 }
 

@@ -130,6 +130,97 @@ __global__ void __launch_bounds__(256) k_sh_grad(DevCam cam, DevCfg g, const flo
   }
 }
 
+// ---------------------------------------------------------------- chunk culling
+// A static cloud in spatial order is cut into chunks of kChunkPoints
+// consecutive points with a bounding box each (k_chunk_bounds, once).  The
+// binning kernels of a view then skip the chunks whose box cannot produce a
+// footprint in the view's frame -- behind the near plane, or projecting
+// wholly outside the image or the screen band (sort-first sharding, SURVEY
+// §8(e)).  One CTA of the projection / scatter kernels covers exactly one
+// chunk.  Conservative: a box crossing the near plane is kept; the projected
+// hull of the 8 corners bounds every interior point (perspective keeps
+// convexity in front of the camera), widened by 2 px for the 2x2 footprint
+// and fp32 rounding.
+constexpr int kChunkPoints = kPointThreads * kPPT;  // 1024
+
+__global__ void __launch_bounds__(kPointThreads) k_chunk_bounds(const float* __restrict__ xyz, int64_t N,
+                                                                float* __restrict__ box) {
+  const int64_t i0 = (int64_t)blockIdx.x * kChunkPoints + threadIdx.x;
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int k = 0; k < kPPT; ++k) {
+    const int64_t i = i0 + k * kPointThreads;
+    if (i >= N) break;
+    const float p[3] = {__ldg(xyz + 3 * i), __ldg(xyz + 3 * i + 1), __ldg(xyz + 3 * i + 2)};
+    if (!(isfinite(p[0]) && isfinite(p[1]) && isfinite(p[2]))) continue;  // never has a footprint
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = fminf(lo[a], p[a]);
+      hi[a] = fmaxf(hi[a], p[a]);
+    }
+  }
+  __shared__ float red[6][kPointThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+    if (lane == 0) {
+      red[a][w] = lo[a];
+      red[3 + a][w] = hi[a];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    float v = red[threadIdx.x][0];
+    for (int q = 1; q < kPointThreads / 32; ++q)
+      v = threadIdx.x < 3 ? fminf(v, red[threadIdx.x][q]) : fmaxf(v, red[threadIdx.x][q]);
+    box[(size_t)blockIdx.x * 6 + threadIdx.x] = v;
+  }
+}
+
+// true when chunk `b`'s box can hold a point with a footprint in the view's
+// frame / band (warp-uniform: lanes 0-7 project the 8 corners, lane 0's
+// reductions are broadcast)
+__device__ __forceinline__ bool chunk_live(const DevCam& cam, const DevCfg& g, const float* __restrict__ box,
+                                           int64_t b) {
+  const int lane = threadIdx.x & 31;
+  const float* bx = box + (size_t)b * 6;
+  const float x0 = __ldg(bx), y0 = __ldg(bx + 1), z0 = __ldg(bx + 2);
+  const float x1 = __ldg(bx + 3), y1 = __ldg(bx + 4), z1 = __ldg(bx + 5);
+  if (!(x0 <= x1 && y0 <= y1 && z0 <= z1)) return false;  // no finite point: no footprint
+  const bool act = lane < 8;
+  const float X = (lane & 1) ? x1 : x0, Y = (lane & 2) ? y1 : y0, Z = (lane & 4) ? z1 : z0;
+  const float xc = cam.R[0] * X + cam.R[1] * Y + cam.R[2] * Z + cam.t[0];
+  const float yc = cam.R[3] * X + cam.R[4] * Y + cam.R[5] * Z + cam.t[1];
+  const float zc = cam.R[6] * X + cam.R[7] * Y + cam.R[8] * Z + cam.t[2];
+  auto allmax = [&](float v) {
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  auto allmin = [&](float v) {
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  // z_c is affine in the point: its extremes over the box are at corners
+  if (allmax(act ? zc : -INFINITY) < cam.z_near * 0.999f) return false;  // all behind the near plane
+  if (!(allmin(act ? zc : INFINITY) > cam.z_near * 1.001f)) return true;  // crosses it: keep
+  const float u = cam.fx * (xc / zc) + cam.cx, v = cam.fy * (yc / zc) + cam.cy;
+  const float umin = allmin(act ? u : INFINITY), umax = allmax(act ? u : -INFINITY);
+  const float vmin = allmin(act ? v : INFINITY), vmax = allmax(act ? v : -INFINITY);
+  if (!(isfinite(umin) && isfinite(umax) && isfinite(vmin) && isfinite(vmax))) return true;
+  // a point's 2x2 block covers pixels floor(u - 1/2) + {0, 1}: within [umin - 1/2, umax + 1/2]
+  const float row_lo = (float)(g.ty0 * kTile), row_hi = (float)min(g.ty1 * kTile, g.H);
+  if (umax + 2.5f < 0.0f || umin - 2.5f >= (float)g.W) return false;
+  if (vmax + 2.5f < row_lo || vmin - 2.5f >= row_hi) return false;
+  return true;
+}
+
 // kPPT points per thread, the position / opacity loads of all of them issued
 // before any compute so enough bytes are in flight to cover HBM latency.
 // Bilinear with a scatter record (the unfused path of large clouds): the
@@ -144,13 +235,20 @@ __global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
     DevCam cam, DevCfg g, const float* __restrict__ xyz, const float* __restrict__ opacity,
     const float* __restrict__ feat, bool pack, int64_t N, PointRec* __restrict__ rec,
     uint32_t* __restrict__ tile_count, uint4* __restrict__ slots, uint32_t* __restrict__ dbg_key,
-    uint32_t* __restrict__ dbg_tiles, float* __restrict__ feat_out, uint2* __restrict__ scat) {
-  const int64_t stride = (int64_t)gridDim.x * kPointThreads;
-  const int64_t i0 = (int64_t)blockIdx.x * kPointThreads + threadIdx.x;
+    uint32_t* __restrict__ dbg_tiles, float* __restrict__ feat_out, uint2* __restrict__ scat,
+    const float* __restrict__ chunk_box, uint8_t* __restrict__ chunk_alive) {
+  // CTA b covers points [b kChunkPoints, (b + 1) kChunkPoints): one chunk
+  const int64_t stride = kPointThreads;
+  const int64_t i0 = (int64_t)blockIdx.x * kChunkPoints + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   // bilinear + scatter record: visible-only writes, warp-aggregated slots
   const bool agg = MODE == 0 && scat != nullptr && tile_count != nullptr;
+  if (agg && chunk_box) {  // the whole chunk is skipped when its box cannot reach the frame / band
+    const bool live = chunk_live(cam, g, chunk_box, blockIdx.x);
+    if (threadIdx.x == 0) chunk_alive[blockIdx.x] = live ? 1 : 0;
+    if (!live) return;
+  }
   float X[kPPT], Y[kPPT], Z[kPPT], O[kPPT];
   float4 Fv[kPPT];
 #pragma unroll
@@ -452,9 +550,10 @@ __global__ void __launch_bounds__(kPointThreads) k_scatter(
 __global__ void __launch_bounds__(kPointThreads) k_scatter_slots(
     DevCfg g, const PointRec* __restrict__ rec, const uint4* __restrict__ slots, int64_t N,
     const uint32_t* __restrict__ ranges, unsigned long long* __restrict__ entries,
-    const uint2* __restrict__ scat) {
-  const int64_t stride = (int64_t)gridDim.x * kPointThreads;
-  const int64_t i0 = (int64_t)blockIdx.x * kPointThreads + threadIdx.x;
+    const uint2* __restrict__ scat, const uint8_t* __restrict__ chunk_alive) {
+  const int64_t stride = kPointThreads;  // CTA b: chunk b, as in k_project_count
+  const int64_t i0 = (int64_t)blockIdx.x * kChunkPoints + threadIdx.x;
+  if (chunk_alive && !chunk_alive[blockIdx.x]) return;
   if (scat) {  // 8 bytes per point (+ 16 per visible point) instead of the 32-byte record
     uint2 q[kPPT];
 #pragma unroll

@@ -274,3 +274,55 @@ def test_rasterize_sh_and_env_arguments(inpc):
     bg = oracle.env_background(c["cams"][0], env, 64, 64)
     r2 = oracle.render(c["cams"][0], c["xyz"], c["feat"], c["opacity"], 64, 64, bg=bg)
     np.testing.assert_allclose(F2[0].cpu().numpy(), r2["F"], atol=IMG_TOL)
+
+
+def test_chunk_bounds_match_numpy(inpc, ctx):
+    c = synthgen.config1(seed=31, N=5000)
+    xyz = c["xyz"].copy()
+    xyz[1030] = np.nan                      # ignored by its chunk's box
+    t = dev(xyz)
+    box = ctx.set_chunks(t)
+    ctx.set_chunks(None)
+    b = box.cpu().numpy()
+    assert b.shape == (5, 6)
+    for k in range(5):
+        p = xyz[k * 1024:(k + 1) * 1024]
+        p = p[np.isfinite(p).all(1)]
+        np.testing.assert_array_equal(b[k, :3], p.min(0))
+        np.testing.assert_array_equal(b[k, 3:], p.max(0))
+
+
+@pytest.mark.parametrize("which", ["cfg4_bands", "cfg5_views"])
+def test_chunk_culling_changes_nothing(inpc, which):
+    """Chunk culling (inpc_ctx_set_chunks) skips whole chunks of the spatially
+    ordered static cloud; tile lists and images must be bit-identical to the
+    unculled raster, for screen bands (cfg 4, sort-first sharding) and for
+    orbit views (cfg 5), and the lists equal the oracle's."""
+    a, b = inpc.Context(0), inpc.Context(0)
+    c = synthgen.config4() if which == "cfg4_bands" else synthgen.config5()
+    xyz0 = dev(c["xyz"])
+    perm = a.spatial_order(xyz0)
+    xyz, feat, op = xyz0[perm].contiguous(), dev(c["feat"])[perm].contiguous(), dev(c["opacity"])[perm].contiguous()
+    del xyz0
+    b.set_chunks(xyz)
+    H, W, C = c["H"], c["W"], c["C"]
+    if which == "cfg4_bands":
+        cases = [(c["cams"][0], band) for band in ((0, 45), (45, 90), (90, 135), (30, 31))]
+    else:
+        cases = [(c["cams"][v], None) for v in (0, 13, 50)]
+    for cam, band in cases:
+        cfg = inpc.make_cfg(H, W, C, band=band)
+        ra = a.forward(cfg, [cam], xyz, feat, op)
+        rb = b.forward(cfg, [cam], xyz, feat, op)
+        ea, eb = a.debug_export(0, H=H, W=W), b.debug_export(0, H=H, W=W)
+        torch.cuda.synchronize()
+        assert torch.equal(ea["tile_ranges"], eb["tile_ranges"])
+        assert torch.equal(ea["sorted_idx"], eb["sorted_idx"])
+        rows = slice(None) if band is None else slice(band[0] * 8, min(band[1] * 8, H))
+        for k in ("F", "A", "D"):      # only the band's rows are written
+            assert torch.equal(ra[k][:, rows], rb[k][:, rows])
+        if band == (45, 90) or (band is None and cam is c["cams"][13]):
+            tr, ti = oracle.tile_lists(cam, xyz.cpu().numpy(), H, W, band=band)
+            np.testing.assert_array_equal(eb["tile_ranges"].cpu().numpy().view(np.uint32), tr)
+            np.testing.assert_array_equal(eb["sorted_idx"].cpu().numpy().view(np.uint32), ti)
+    a.close(); b.close()
