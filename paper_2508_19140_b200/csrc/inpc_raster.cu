@@ -791,11 +791,11 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     }
     if (!fused_kp) {
       StageTimer tm(c, s, kStScan, 1);
+      uint32_t* ht = c->no_mid_sort ? nullptr : (uint32_t*)c->huge_tiles.p;
       k_scan_tiles<<<scan_blocks, kScanThreads, 0, s>>>(T, tc, (uint32_t*)vs.ranges.p,
                                                         (uint32_t*)c->cursor.p,
                                                         (uint32_t*)c->big_tiles.p, scan_state, scan_ctl,
-                                                        sc, c->no_mid_sort ? nullptr : (uint32_t*)c->huge_tiles.p,
-                                                        (uint32_t)kMidMax);
+                                                        sc, ht, (uint32_t)kMidMax);
       CK(cudaGetLastError());
     }
     uint64_t need = bound;

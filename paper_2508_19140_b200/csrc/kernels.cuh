@@ -471,24 +471,42 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
     }
   }
   __syncthreads();
-  uint32_t off = s_prefix + excl;
+  uint32_t off = s_prefix + excl, mxh = 0u;
+  const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    if (i0 + k < T) {
+    const bool in = i0 + k < T;
+    if (in) {
       ranges[i0 + k] = off;
       cursor[i0 + k] = off;
-      if (c[k] > (uint32_t)kWarpSortCap) {
-        big_tiles[atomicAdd(&sc->num_big, 1u)] = i0 + k;
+    }
+    // big-tile lists: one atomic per warp and item (the list order is free)
+    const bool big = in && c[k] > (uint32_t)kWarpSortCap;
+    const unsigned bm = __ballot_sync(0xffffffffu, big);
+    if (bm) {
+      uint32_t base = 0u;
+      if (lane == __ffs(bm) - 1) base = atomicAdd(&sc->num_big, (uint32_t)__popc(bm));
+      base = __shfl_sync(0xffffffffu, base, __ffs(bm) - 1);
+      if (big) {
+        big_tiles[base + __popc(bm & lt)] = i0 + k;
         mx = max(mx, c[k]);
-        if (huge_tiles && c[k] > huge_min) {  // also on k_sort_big's own list
-          huge_tiles[atomicAdd(&sc->num_huge, 1u)] = i0 + k;
-          atomicMax(&sc->max_huge, c[k]);
+      }
+      const bool huge = big && huge_tiles && c[k] > huge_min;  // also on k_sort_big's own list
+      const unsigned hm = __ballot_sync(0xffffffffu, huge);
+      if (hm) {
+        uint32_t hb = 0u;
+        if (lane == __ffs(hm) - 1) hb = atomicAdd(&sc->num_huge, (uint32_t)__popc(hm));
+        hb = __shfl_sync(0xffffffffu, hb, __ffs(hm) - 1);
+        if (huge) {
+          huge_tiles[hb + __popc(hm & lt)] = i0 + k;
+          mxh = max(mxh, c[k]);
         }
       }
     }
     off += c[k];
   }
   if (mx) atomicMax(&sc->max_big, mx);
+  if (mxh) atomicMax(&sc->max_huge, mxh);
   if (i0 < T && i0 + kScanItems >= T) {  // the thread owning the last tile
     ranges[T] = off;
     sc->Ft = off;
