@@ -56,6 +56,14 @@ const char* kStageNames[kNumStages] = {"memset",    "project_count", "scan_tiles
                                        "sort_big",  "blend_fwd",     "blend_bwd",  "bin_fused",
                                        "sh_grad",   "single_sort",   "sort_mid"};
 
+// Per-view scratch of the binning (stream ordered).  Two sets, so that two
+// views can be in flight on the context's two internal streams.
+struct Scratch {
+  Buf scat;  // unfused bilinear binning: depth key + tile block | corner mask per point
+  Buf zeroed, cursor, big_tiles, huge_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg, g_eval;
+  Buf chunk_alive;
+};
+
 struct ViewState {
   Buf ranges, sorted_idx, T_final, last, dbg_key, dbg_tiles, scalars, rec, feat_eval;
   uint64_t idx_cap = 0;
@@ -78,10 +86,12 @@ struct inpc_ctx {
   const float* chunk_box = nullptr;
   const float* chunk_xyz = nullptr;
   int64_t chunk_N = 0;
-  Buf chunk_alive;
-  // scratch (shared by views, stream ordered)
-  Buf scat;  // unfused bilinear binning: depth key + tile block | corner mask per point
-  Buf zeroed, cursor, big_tiles, huge_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg, g_eval;
+  // scratch: two sets (views alternate between the two internal streams)
+  static constexpr int kMaxViewStreams = 4;
+  Scratch scr[kMaxViewStreams];
+  cudaStream_t vstream[kMaxViewStreams] = {};  // internal non-blocking streams for multi-view calls
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxViewStreams] = {};
+  int view_streams = 2;                        // env INPC_VIEW_STREAMS (1 = one stream, A/B)
   Buf f4_rec, f4_keys, f4_vals, f4_keys2, f4_vals2, f4_hist, f4_scan, f4_misc;  // NEXT f4 baseline
   int bin_grid[3] = {0, 0, 0};  // cooperative grid of k_bin_bilinear<2,4,8>
   bool no_fused_bin = false;     // env INPC_NO_FUSED_BIN=1: separate binning kernels
@@ -178,9 +188,12 @@ struct AllocScope {
 };
 
 void release_all(inpc_ctx* c) {
-  for (Buf* b : {&c->chunk_alive, &c->scat, &c->zeroed, &c->cursor, &c->big_tiles, &c->huge_tiles, &c->big_elem, &c->big_chunk, &c->entries, &c->slots,
-                 &c->agg, &c->g_eval, &c->tmp, &c->overflow, &c->f4_rec, &c->f4_keys, &c->f4_vals,
-                 &c->f4_keys2, &c->f4_vals2, &c->f4_hist, &c->f4_scan, &c->f4_misc})
+  for (Scratch& x : c->scr)
+    for (Buf* b : {&x.chunk_alive, &x.scat, &x.zeroed, &x.cursor, &x.big_tiles, &x.huge_tiles, &x.big_elem,
+                   &x.big_chunk, &x.entries, &x.slots, &x.agg, &x.g_eval, &x.tmp, &x.overflow})
+      free_buf(*b);
+  for (Buf* b : {&c->f4_rec, &c->f4_keys, &c->f4_vals, &c->f4_keys2, &c->f4_vals2, &c->f4_hist, &c->f4_scan,
+                 &c->f4_misc})
     free_buf(*b);
   for (auto& v : c->views)
     for (Buf* b : {&v.ranges, &v.sorted_idx, &v.T_final, &v.last, &v.dbg_key, &v.dbg_tiles, &v.scalars,
@@ -510,6 +523,17 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
     const char* e = getenv("INPC_NO_FUSED_BIN");
     c->no_fused_bin = e && e[0] == '1';
   }
+  {
+    const char* e = getenv("INPC_VIEW_STREAMS");
+    c->view_streams = e ? atoi(e) : 2;
+    if (c->view_streams < 1) c->view_streams = 1;
+    if (c->view_streams > inpc_ctx::kMaxViewStreams) c->view_streams = inpc_ctx::kMaxViewStreams;
+  }
+  for (int k = 0; k < inpc_ctx::kMaxViewStreams; ++k) {
+    cudaStreamCreateWithFlags(&c->vstream[k], cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   if (cudaMallocHost(&c->host_scalars, 64) != cudaSuccess) {
     cudaGetLastError();
     delete c;
@@ -532,6 +556,11 @@ int inpc_ctx_destroy(inpc_ctx* c) {
     cudaEventDestroy(e.b);
   }
   for (auto e : c->pool) cudaEventDestroy(e);
+  for (int k = 0; k < inpc_ctx::kMaxViewStreams; ++k) {
+    if (c->vstream[k]) cudaStreamDestroy(c->vstream[k]);
+    if (c->ev_join[k]) cudaEventDestroy(c->ev_join[k]);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->host_scalars) cudaFreeHost(c->host_scalars);
   delete c;
   return INPC_OK;
@@ -652,23 +681,75 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   // k_scan_tiles leaves them zero after every call
   const size_t zero_bytes = count_bytes + (size_t)scan_blocks * 8 + sizeof(ScanCtl);
   bool fresh = false;
-  if ((st = ensure(c->zeroed, zero_bytes, s, &fresh))) return st;
-  if (fresh) CK(cudaMemsetAsync(c->zeroed.p, 0, c->zeroed.bytes, s));
-  if ((st = ensure(c->cursor, (size_t)(T + 1) * 4, s))) return st;
-  if (!gauss && (st = ensure(c->slots, (size_t)(N > 0 ? N : 1) * 16, s))) return st;
-  if ((st = ensure(c->big_tiles, (size_t)(T + 1) * 4, s))) return st;
-  if ((st = ensure(c->huge_tiles, (size_t)(T + 1) * 4, s))) return st;
-  if ((st = ensure(c->big_elem, (size_t)(T + 2) * 4, s))) return st;
-  if ((st = ensure(c->big_chunk, (size_t)(T + 2) * 4, s))) return st;
-  if ((st = ensure(c->overflow, 64, s, &fresh))) return st;  // [0] Gaussian overflow flag, [6] k_sort_mid done counter
-  if (fresh) CK(cudaMemsetAsync(c->overflow.p, 0, c->overflow.bytes, s));
   uint64_t bound = gauss ? 0 : 4ull * (uint64_t)N;  // bilinear: <= 4 tiles per point
   if (!gauss && bound >= 0xFFFFFFFFull) return INPC_KEY_OVERFLOW;
   if ((int)c->views.size() < V) c->views.resize(V);
   c->have_state = false;
-
+  const int nblk = (int)((N + (int64_t)kPointThreads * kPPT - 1) / ((int64_t)kPointThreads * kPPT));
+  // bilinear: one cooperative launch for H1-H6 when the points fit in registers
+  // (measured on cfg 2 at 1080p: fused 58.5 us vs 67 us for the separate
+  // kernels eagerly, and 201.5 vs 203.7 us per fwd+bwd step in a CUDA graph)
+  int fused_kp = 0, fused_grid = 0;
+  if (!gauss && !sh && N > 0 && !c->no_fused_bin && T < (1 << 28)) {  // tile base + corner mask in 32 bits
+    const int kps[3] = {2, 4, 8};
+    for (int q = 0; q < 3; ++q)
+      if (c->bin_grid[q] > 0 && N <= (int64_t)kps[q] * c->bin_grid[q] * kBinThreads) {
+        fused_kp = kps[q];
+        fused_grid = c->bin_grid[q];
+        break;
+      }
+  }
+  // entry capacity per view: bilinear 4N; Gaussian a static bound when it
+  // fits a quarter of the free memory (sync-free), else F_t read back per view
+  std::vector<uint64_t> need_v(V, bound);
+  bool sync_views = false;
+  if (gauss) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+      cudaGetLastError();
+      free_b = 0;
+    }
+    for (int v = 0; v < V; ++v) {
+      DevCam dv;
+      DevCfg gv;
+      make_dev(cfg, cams[v], dv, gv);
+      const uint64_t per_pt = gauss_tiles_bound(cfg, cams[v], gv.ty1 - gv.ty0, gv.tiles_x);
+      const uint64_t ub = per_pt * (uint64_t)N;
+      const bool have = c->views[v].idx_cap >= ub;  // already sized for the bound
+      if (per_pt && ub < 0xFFFFFFFFull && (have || ub * 20ull <= (uint64_t)(free_b / 4))) need_v[v] = ub;
+      else sync_views = true;
+    }
+  }
+  // views alternate between the two internal streams (fork / join on the
+  // caller's stream, graph-capturable): one view's latency-bound kernels and
+  // kernel tails overlap the other's; not while profiling (per-stage event
+  // times stay per kernel), not with the per-view F_t read-back
+  const int nsets = (V > 1 && N > 0 && !sync_views && !c->profiling) ? (V < c->view_streams ? V : c->view_streams) : 1;
+  const bool fork = nsets > 1;
+  uint64_t need_max = 1;
+  for (int v = 0; v < V; ++v) need_max = need_v[v] > need_max ? need_v[v] : need_max;
+  for (int k = 0; k < nsets; ++k) {
+    Scratch& X = c->scr[k];
+    if ((st = ensure(X.zeroed, zero_bytes, s, &fresh))) return st;
+    if (fresh) CK(cudaMemsetAsync(X.zeroed.p, 0, X.zeroed.bytes, s));
+    if ((st = ensure(X.cursor, (size_t)(T + 1) * 4, s))) return st;
+    if (!gauss && (st = ensure(X.slots, (size_t)(N > 0 ? N : 1) * 16, s))) return st;
+    if ((st = ensure(X.big_tiles, (size_t)(T + 1) * 4, s))) return st;
+    if ((st = ensure(X.huge_tiles, (size_t)(T + 1) * 4, s))) return st;
+    if ((st = ensure(X.big_elem, (size_t)(T + 2) * 4, s))) return st;
+    if ((st = ensure(X.big_chunk, (size_t)(T + 2) * 4, s))) return st;
+    // [0] Gaussian overflow flag, [6] k_sort_mid done counter
+    if ((st = ensure(X.overflow, 64, s, &fresh))) return st;
+    if (fresh) CK(cudaMemsetAsync(X.overflow.p, 0, X.overflow.bytes, s));
+    if (!sync_views) {
+      if ((st = ensure(X.entries, (size_t)need_max * 8, s))) return st;
+      if ((st = ensure(X.tmp, (size_t)need_max * 8, s))) return st;
+    }
+    if (N > 0 && !fused_kp && !gauss && T < (1 << 28) && (st = ensure(X.scat, (size_t)N * 8, s))) return st;
+    if (fused_kp && (st = ensure(X.agg, (size_t)fused_grid * 4, s))) return st;
+    if ((st = ensure(X.chunk_alive, (size_t)(nblk > 0 ? nblk : 1), s))) return st;
+  }
   for (int v = 0; v < V; ++v) {
-    make_dev(cfg, cams[v], dc, g);
     ViewState& vs = c->views[v];
     if ((st = ensure(vs.ranges, (size_t)(T + 1) * 4, s))) return st;
     if ((st = ensure(vs.T_final, (size_t)P * 4, s))) return st;
@@ -680,50 +761,42 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       if ((st = ensure(vs.dbg_key, (size_t)N * 4, s))) return st;
       if ((st = ensure(vs.dbg_tiles, (size_t)N * 4, s))) return st;
     }
+    if (sh && !packed && N > 0 && (st = ensure(vs.feat_eval, (size_t)N * cfg->C * 4, s))) return st;
+    if (!sync_views) {
+      if ((st = ensure(vs.sorted_idx, (size_t)(need_v[v] ? need_v[v] : 1) * 4, s))) return st;
+      vs.idx_cap = need_v[v];
+    }
+  }
+  if (fork) {
+    CK(cudaEventRecord(c->ev_fork, s));
+    for (int k = 0; k < nsets; ++k) CK(cudaStreamWaitEvent(c->vstream[k], c->ev_fork, 0));
+  }
+
+  for (int v = 0; v < V; ++v) {
+    make_dev(cfg, cams[v], dc, g);
+    ViewState& vs = c->views[v];
+    Scratch& X = c->scr[v % nsets];
+    const cudaStream_t sv = fork ? c->vstream[v % nsets] : s;
     const float* feat_v = feat + (size_t)v * feat_view_stride;
     const float* bg_v = bg ? bg + (size_t)v * bg_view_stride : nullptr;
-    float* feat_out = nullptr;  // SH features evaluated for this view (when not packed)
-    if (sh && !packed && N > 0) {
-      if ((st = ensure(vs.feat_eval, (size_t)N * cfg->C * 4, s))) return st;
-      feat_out = (float*)vs.feat_eval.p;
-    }
+    float* feat_out = (sh && !packed && N > 0) ? (float*)vs.feat_eval.p : nullptr;  // SH features of this view
     const float* feat_blend = feat_out ? feat_out : feat_v;
-    uint32_t* tc = (uint32_t*)c->zeroed.p;
-    unsigned long long* scan_state = (unsigned long long*)((char*)c->zeroed.p + count_bytes);
+    uint32_t* tc = (uint32_t*)X.zeroed.p;
+    unsigned long long* scan_state = (unsigned long long*)((char*)X.zeroed.p + count_bytes);
     ScanCtl* scan_ctl = (ScanCtl*)(scan_state + scan_blocks);
     ViewScalars* sc = (ViewScalars*)vs.scalars.p;
-    const int nblk = (int)((N + (int64_t)kPointThreads * kPPT - 1) / ((int64_t)kPointThreads * kPPT));
-    // bilinear: one cooperative launch for H1-H6 when the points fit in registers
-    // (measured on cfg 2 at 1080p: fused 58.5 us vs 67 us for the separate
-    // kernels eagerly, and 201.5 vs 203.7 us per fwd+bwd step in a CUDA graph)
-    int fused_kp = 0, fused_grid = 0;
-    if (!gauss && !sh && N > 0 && !c->no_fused_bin && T < (1 << 28)) {  // tile base + corner mask in 32 bits
-      const int kps[3] = {2, 4, 8};
-      for (int q = 0; q < 3; ++q)
-        if (c->bin_grid[q] > 0 && N <= (int64_t)kps[q] * c->bin_grid[q] * kBinThreads) {
-          fused_kp = kps[q];
-          fused_grid = c->bin_grid[q];
-          break;
-        }
-    }
     uint32_t* dk = debug ? (uint32_t*)vs.dbg_key.p : nullptr;
     uint32_t* dt = debug ? (uint32_t*)vs.dbg_tiles.p : nullptr;
     if (fused_kp) {
-      const uint64_t need = bound;
-      if ((st = ensure(c->entries, (size_t)need * 8, s))) return st;
-      if ((st = ensure(c->tmp, (size_t)need * 8, s))) return st;
-      if ((st = ensure(vs.sorted_idx, (size_t)need * 4, s))) return st;
-      if ((st = ensure(c->agg, (size_t)fused_grid * 4, s))) return st;
-      vs.idx_cap = need;
-      StageTimer tm(c, s, kStBin, 1);
+      StageTimer tm(c, sv, kStBin, 1);
       PointRec* recp = (PointRec*)vs.rec.p;
       uint32_t* rg = (uint32_t*)vs.ranges.p;
-      uint32_t* ag = (uint32_t*)c->agg.p;
-      uint32_t* bt = (uint32_t*)c->big_tiles.p;
-      uint32_t* be = (uint32_t*)c->big_elem.p;
-      uint32_t* bc = (uint32_t*)c->big_chunk.p;
-      unsigned long long* en = (unsigned long long*)c->entries.p;
-      unsigned long long* tp = (unsigned long long*)c->tmp.p;
+      uint32_t* ag = (uint32_t*)X.agg.p;
+      uint32_t* bt = (uint32_t*)X.big_tiles.p;
+      uint32_t* be = (uint32_t*)X.big_elem.p;
+      uint32_t* bc = (uint32_t*)X.big_chunk.p;
+      unsigned long long* en = (unsigned long long*)X.entries.p;
+      unsigned long long* tp = (unsigned long long*)X.tmp.p;
       uint32_t* si = (uint32_t*)vs.sorted_idx.p;
       int Ti = T;
       int64_t Nn = N;
@@ -738,16 +811,16 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
 #ifdef INPC_PHASE_TIMES
       {
         unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        cudaMemcpyToSymbolAsync(g_bin_ts, z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
+        cudaMemcpyToSymbolAsync(g_bin_ts, z, sizeof(z), 0, cudaMemcpyHostToDevice, sv);
       }
 #endif
       const size_t bsm = fused_kp == 2 ? bin_smem_bytes<2>() : fused_kp == 4 ? bin_smem_bytes<4>() : bin_smem_bytes<8>();
-      CK(cudaLaunchCooperativeKernel(fn, fused_grid, kBinThreads, args, bsm, s));
+      CK(cudaLaunchCooperativeKernel(fn, fused_grid, kBinThreads, args, bsm, sv));
 #ifdef INPC_PHASE_TIMES
       {
         unsigned long long ts[8];
-        cudaMemcpyFromSymbolAsync(ts, g_bin_ts, sizeof(ts), 0, cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
+        cudaMemcpyFromSymbolAsync(ts, g_bin_ts, sizeof(ts), 0, cudaMemcpyDeviceToHost, sv);
+        cudaStreamSynchronize(sv);
         fprintf(stderr, "bin phases us: project %.1f scan %.1f scatter %.1f prefix %.1f chunks %.1f end %.1f\n",
                 (ts[1] - ts[0]) * 1e-3, (ts[2] - ts[1]) * 1e-3, (ts[3] - ts[2]) * 1e-3,
                 ts[4] ? (ts[4] - ts[3]) * 1e-3 : 0.0, ts[5] ? (ts[5] - ts[3]) * 1e-3 : 0.0,
@@ -755,102 +828,74 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       }
 #endif
     }
-    uint2* scp = nullptr;  // bilinear: compact per-point scatter data (tile block + mask in 32 bits)
-    if (N > 0 && !fused_kp && !gauss && T < (1 << 28)) {
-      if ((st = ensure(c->scat, (size_t)N * 8, s))) return st;
-      scp = (uint2*)c->scat.p;
-    }
+    // bilinear: compact per-point scatter data (tile block + mask in 32 bits)
+    uint2* scp = (N > 0 && !fused_kp && !gauss && T < (1 << 28)) ? (uint2*)X.scat.p : nullptr;
     // chunk culling: bilinear unfused path over the cloud the bounds describe (not in
     // debug mode, whose per-point exports cover every point)
     const float* cbox = (scp && !gauss && !debug && c->chunk_box && c->chunk_xyz == xyz && c->chunk_N == N)
                             ? c->chunk_box : nullptr;
-    uint8_t* calive = nullptr;
-    if (cbox) {
-      if ((st = ensure(c->chunk_alive, (size_t)nblk, s))) return st;
-      calive = (uint8_t*)c->chunk_alive.p;
-    }
+    uint8_t* calive = cbox ? (uint8_t*)X.chunk_alive.p : nullptr;
     if (N > 0 && !fused_kp) {
-      StageTimer tm(c, s, kStProject, 1);
+      StageTimer tm(c, sv, kStProject, 1);
       PointRec* recp = (PointRec*)vs.rec.p;
-      uint4* slp = (uint4*)c->slots.p;
+      uint4* slp = (uint4*)X.slots.p;
       if (gauss && sh)
-        k_project_count<1, true><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N, recp,
-                                                                 tc, nullptr, dk, dt, feat_out, nullptr,
-                                                                 nullptr, nullptr);
-      else if (gauss)
-        k_project_count<1, false><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, false, N, recp,
+        k_project_count<1, true><<<nblk, kPointThreads, 0, sv>>>(dc, g, xyz, opacity, feat_v, false, N, recp,
                                                                   tc, nullptr, dk, dt, feat_out, nullptr,
                                                                   nullptr, nullptr);
+      else if (gauss)
+        k_project_count<1, false><<<nblk, kPointThreads, 0, sv>>>(dc, g, xyz, opacity, feat_v, false, N, recp,
+                                                                   tc, nullptr, dk, dt, feat_out, nullptr,
+                                                                   nullptr, nullptr);
       else if (sh)
-        k_project_count<0, true><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N, recp,
-                                                                 tc, slp, dk, dt, feat_out, scp, cbox, calive);
-      else
-        k_project_count<0, false><<<nblk, kPointThreads, 0, s>>>(dc, g, xyz, opacity, feat_v, packed, N, recp,
+        k_project_count<0, true><<<nblk, kPointThreads, 0, sv>>>(dc, g, xyz, opacity, feat_v, packed, N, recp,
                                                                   tc, slp, dk, dt, feat_out, scp, cbox, calive);
+      else
+        k_project_count<0, false><<<nblk, kPointThreads, 0, sv>>>(dc, g, xyz, opacity, feat_v, packed, N, recp,
+                                                                   tc, slp, dk, dt, feat_out, scp, cbox, calive);
       CK(cudaGetLastError());
     }
     if (!fused_kp) {
-      StageTimer tm(c, s, kStScan, 1);
-      uint32_t* ht = c->no_mid_sort ? nullptr : (uint32_t*)c->huge_tiles.p;
-      k_scan_tiles<<<scan_blocks, kScanThreads, 0, s>>>(T, tc, (uint32_t*)vs.ranges.p,
-                                                        (uint32_t*)c->cursor.p,
-                                                        (uint32_t*)c->big_tiles.p, scan_state, scan_ctl,
-                                                        sc, ht, (uint32_t)kMidMax);
+      StageTimer tm(c, sv, kStScan, 1);
+      uint32_t* ht = c->no_mid_sort ? nullptr : (uint32_t*)X.huge_tiles.p;
+      k_scan_tiles<<<scan_blocks, kScanThreads, 0, sv>>>(T, tc, (uint32_t*)vs.ranges.p, (uint32_t*)X.cursor.p,
+                                                         (uint32_t*)X.big_tiles.p, scan_state, scan_ctl, sc, ht,
+                                                         (uint32_t)kMidMax);
       CK(cudaGetLastError());
     }
-    uint64_t need = bound;
-    if (gauss) {
-      // the one data-dependent size.  Sync-free (graph-capturable) when a
-      // static bound of the entry count fits the memory budget (a quarter of
-      // the free device memory): the buffers are sized for the bound;
-      // otherwise F_t is read back once per view
-      const uint64_t per_pt = gauss_tiles_bound(cfg, cams[v], g.ty1 - g.ty0, g.tiles_x);
-      const uint64_t ub = per_pt * (uint64_t)N;
-      size_t free_b = 0, total_b = 0;
-      if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
-        cudaGetLastError();
-        free_b = 0;
-      }
-      const bool have = vs.idx_cap >= ub;  // already sized for the bound
-      if (per_pt && ub < 0xFFFFFFFFull && (have || ub * 20ull <= (uint64_t)(free_b / 4))) {
-        need = ub;
-      } else {
-        CK(cudaMemcpyAsync(c->host_scalars, sc, sizeof(ViewScalars), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        need = c->host_scalars[0];
-        if (need >= 0xFFFFFFFFull) return INPC_KEY_OVERFLOW;
-      }
-    }
-    if (!fused_kp) {
-      if ((st = ensure(c->entries, (size_t)(need ? need : 1) * 8, s))) return st;
-      if ((st = ensure(c->tmp, (size_t)(need ? need : 1) * 8, s))) return st;
-      if ((st = ensure(vs.sorted_idx, (size_t)(need ? need : 1) * 4, s))) return st;
+    uint64_t need = need_v[v];
+    if (gauss && sync_views) {  // read F_t back (a huge world sigma has no useful bound)
+      CK(cudaMemcpyAsync(c->host_scalars, sc, sizeof(ViewScalars), cudaMemcpyDeviceToHost, sv));
+      CK(cudaStreamSynchronize(sv));
+      need = c->host_scalars[0];
+      if (need >= 0xFFFFFFFFull) return INPC_KEY_OVERFLOW;
+      if ((st = ensure(X.entries, (size_t)(need ? need : 1) * 8, sv))) return st;
+      if ((st = ensure(X.tmp, (size_t)(need ? need : 1) * 8, sv))) return st;
+      if ((st = ensure(vs.sorted_idx, (size_t)(need ? need : 1) * 4, sv))) return st;
       vs.idx_cap = need;
     }
     if (N > 0 && !fused_kp) {
-      StageTimer tm(c, s, kStScatter, 1);
+      StageTimer tm(c, sv, kStScatter, 1);
       if (gauss)
-        k_scatter<1><<<nblk, kPointThreads, 0, s>>>(g, (const PointRec*)vs.rec.p, N, (uint32_t*)c->cursor.p,
-                                          (unsigned long long*)c->entries.p, need,
-                                          (uint32_t*)c->overflow.p);
+        k_scatter<1><<<nblk, kPointThreads, 0, sv>>>(g, (const PointRec*)vs.rec.p, N, (uint32_t*)X.cursor.p,
+                                                     (unsigned long long*)X.entries.p, need,
+                                                     (uint32_t*)X.overflow.p);
       else
-        k_scatter_slots<<<nblk, kPointThreads, 0, s>>>(g, (const PointRec*)vs.rec.p,
-                                                       (const uint4*)c->slots.p, N,
-                                                       (const uint32_t*)vs.ranges.p,
-                                                       (unsigned long long*)c->entries.p, scp, calive);
+        k_scatter_slots<<<nblk, kPointThreads, 0, sv>>>(g, (const PointRec*)vs.rec.p, (const uint4*)X.slots.p, N,
+                                                        (const uint32_t*)vs.ranges.p,
+                                                        (unsigned long long*)X.entries.p, scp, calive);
       CK(cudaGetLastError());
     }
     if (N > kWarpSortCap && !fused_kp && !c->no_mid_sort) {  // tiles of 257..kMidMax entries
-      StageTimer tm(c, s, kStSortMid, 1);
-      k_sort_mid<<<c->mid_grid, kMidThreads, 0, s>>>((const uint32_t*)vs.ranges.p,
-                                                     (const uint32_t*)c->big_tiles.p, sc,
-                                                     (const unsigned long long*)c->entries.p,
-                                                     (uint32_t*)vs.sorted_idx.p, (uint32_t*)c->overflow.p + 6);
+      StageTimer tm(c, sv, kStSortMid, 1);
+      k_sort_mid<<<c->mid_grid, kMidThreads, 0, sv>>>((const uint32_t*)vs.ranges.p, (const uint32_t*)X.big_tiles.p,
+                                                      sc, (const unsigned long long*)X.entries.p,
+                                                      (uint32_t*)vs.sorted_idx.p, (uint32_t*)X.overflow.p + 6);
       CK(cudaGetLastError());
 #ifdef INPC_PHASE_TIMES
       {
         unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t[8];
-        cudaStreamSynchronize(s);
+        cudaStreamSynchronize(sv);
         cudaMemcpyFromSymbol(t, g_mid_cyc, sizeof(t));
         cudaMemcpyToSymbol(g_mid_cyc, z, sizeof(z));
         const double nt = t[6] ? (double)t[6] : 1.0;
@@ -860,24 +905,24 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
 #endif
     }
     if (N > kWarpSortCap && !fused_kp) {  // a tile can only exceed the cap with > cap points
-      StageTimer tm(c, s, kStSortBig, 1);
+      StageTimer tm(c, sv, kStSortBig, 1);
       uint32_t min_n = c->no_mid_sort ? (uint32_t)kWarpSortCap : (uint32_t)kMidMax;
       const uint32_t* r = (const uint32_t*)vs.ranges.p;
-      const uint32_t* bt = (const uint32_t*)c->big_tiles.p;
-      uint32_t* be = (uint32_t*)c->big_elem.p;
-      uint32_t* bc = (uint32_t*)c->big_chunk.p;
+      const uint32_t* bt = (const uint32_t*)X.big_tiles.p;
+      uint32_t* be = (uint32_t*)X.big_elem.p;
+      uint32_t* bc = (uint32_t*)X.big_chunk.p;
       ViewScalars* scc = sc;
-      unsigned long long* en = (unsigned long long*)c->entries.p;
-      unsigned long long* tp = (unsigned long long*)c->tmp.p;
+      unsigned long long* en = (unsigned long long*)X.entries.p;
+      unsigned long long* tp = (unsigned long long*)X.tmp.p;
       uint32_t* si = (uint32_t*)vs.sorted_idx.p;
-      const uint32_t* ht = (const uint32_t*)c->huge_tiles.p;
+      const uint32_t* ht = (const uint32_t*)X.huge_tiles.p;
       void* args[] = {(void*)&r, (void*)&bt, (void*)&be, (void*)&bc, (void*)&scc, (void*)&en, (void*)&tp, (void*)&si,
                       (void*)&min_n, (void*)&ht};
       CK(cudaLaunchCooperativeKernel((void*)k_sort_big, c->big_grid, kBigThreadsLarge, args,
-                                     (size_t)kBigChunkLarge * 8 + kRadixSmemU32 * 4, s));
+                                     (size_t)kBigChunkLarge * 8 + kRadixSmemU32 * 4, sv));
     }
     {
-      StageTimer tm(c, s, kStBlendFwd, 1);
+      StageTimer tm(c, sv, kStBlendFwd, 1);
       BlendOut o;
       o.F = out_feat + (size_t)v * P * cfg->C;
       o.A = out_alpha ? out_alpha + (size_t)v * P : nullptr;
@@ -888,14 +933,20 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       o.last = (uint32_t*)vs.last.p;
       const bool pf = N < kFwdPrefetchMaxDensity * (int64_t)T;
       if (gauss)
-        dispatch_blend_fwd<1>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_blend, false, bg_v,
-                              (const uint32_t*)vs.ranges.p, (const unsigned long long*)c->entries.p,
+        dispatch_blend_fwd<1>(cmax, band_tiles, sv, dc, g, (const PointRec*)vs.rec.p, feat_blend, false, bg_v,
+                              (const uint32_t*)vs.ranges.p, (const unsigned long long*)X.entries.p,
                               (uint32_t*)vs.sorted_idx.p, o, pf);
       else
-        dispatch_blend_fwd<0>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_blend, packed, bg_v,
-                              (const uint32_t*)vs.ranges.p, (const unsigned long long*)c->entries.p,
+        dispatch_blend_fwd<0>(cmax, band_tiles, sv, dc, g, (const PointRec*)vs.rec.p, feat_blend, packed, bg_v,
+                              (const uint32_t*)vs.ranges.p, (const unsigned long long*)X.entries.p,
                               (uint32_t*)vs.sorted_idx.p, o, pf);
       CK(cudaGetLastError());
+    }
+  }
+  if (fork) {
+    for (int k = 0; k < nsets; ++k) {
+      CK(cudaEventRecord(c->ev_join[k], c->vstream[k]));
+      CK(cudaStreamWaitEvent(s, c->ev_join[k], 0));
     }
   }
   c->have_state = true;
@@ -958,9 +1009,20 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   const bool gauss = cfg->splat_mode == INPC_SPLAT_GAUSSIAN;
   const int cmax = cmax_for(cfg->C);
   const bool packed = !gauss && cfg->C == 4;
+  const int nsets = (V > 1 && !c->profiling) ? (V < c->view_streams ? V : c->view_streams) : 1;
+  const bool fork = nsets > 1;
+  if (sh)
+    for (int k = 0; k < nsets; ++k)
+      if ((st = ensure(c->scr[k].g_eval, (size_t)N * cfg->C * 4, s))) return st;
+  if (fork) {
+    CK(cudaEventRecord(c->ev_fork, s));
+    for (int k = 0; k < nsets; ++k) CK(cudaStreamWaitEvent(c->vstream[k], c->ev_fork, 0));
+  }
   for (int v = 0; v < V; ++v) {
     make_dev(cfg, cams[v], dc, g);
     ViewState& vs = c->views[v];
+    Scratch& X = c->scr[v % nsets];
+    const cudaStream_t sv = fork ? c->vstream[v % nsets] : s;
     BwdIn in;
     in.gF = g_feat + (size_t)v * P * cfg->C;
     in.gA = g_alpha ? g_alpha + (size_t)v * P : nullptr;
@@ -973,30 +1035,35 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     const float* bg_v = bg ? bg + (size_t)v * bg_view_stride : nullptr;
     if (sh) {
       // dL/df of this view into a scratch [N, C], then to the SH coefficients
-      if ((st = ensure(c->g_eval, (size_t)N * cfg->C * 4, s))) return st;
-      CK(cudaMemsetAsync(c->g_eval.p, 0, (size_t)N * cfg->C * 4, s));
-      in.g_feat = (float*)c->g_eval.p;
+      CK(cudaMemsetAsync(X.g_eval.p, 0, (size_t)N * cfg->C * 4, sv));
+      in.g_feat = (float*)X.g_eval.p;
       if (!packed) feat_v = (const float*)vs.feat_eval.p;
     }
     {
-      StageTimer tm(c, s, kStBlendBwd, 1);
+      StageTimer tm(c, sv, kStBlendBwd, 1);
       if (gauss)
-        dispatch_blend_bwd<1>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, false, bg_v,
+        dispatch_blend_bwd<1>(cmax, band_tiles, sv, dc, g, (const PointRec*)vs.rec.p, feat_v, false, bg_v,
                               (const uint32_t*)vs.ranges.p, (const uint32_t*)vs.sorted_idx.p, in);
       else
-        dispatch_blend_bwd<0>(cmax, band_tiles, s, dc, g, (const PointRec*)vs.rec.p, feat_v, packed, bg_v,
+        dispatch_blend_bwd<0>(cmax, band_tiles, sv, dc, g, (const PointRec*)vs.rec.p, feat_v, packed, bg_v,
                               (const uint32_t*)vs.ranges.p, (const uint32_t*)vs.sorted_idx.p, in);
       CK(cudaGetLastError());
     }
     if (sh) {
-      StageTimer tm(c, s, kStShGrad, 1);
+      StageTimer tm(c, sv, kStShGrad, 1);
       float* gsh = g_point_feat + (size_t)v * feat_view_stride;
       const unsigned nb = (unsigned)((N + kShPts - 1) / kShPts);
       if (cfg->C == 4 && ((uintptr_t)gsh & 15u) == 0)
-        k_sh_grad<4><<<nb, 256, 0, s>>>(dc, g, xyz, N, (const float*)c->g_eval.p, gsh);
+        k_sh_grad<4><<<nb, 256, 0, sv>>>(dc, g, xyz, N, (const float*)X.g_eval.p, gsh);
       else
-        k_sh_grad<0><<<nb, 256, 0, s>>>(dc, g, xyz, N, (const float*)c->g_eval.p, gsh);
+        k_sh_grad<0><<<nb, 256, 0, sv>>>(dc, g, xyz, N, (const float*)X.g_eval.p, gsh);
       CK(cudaGetLastError());
+    }
+  }
+  if (fork) {
+    for (int k = 0; k < nsets; ++k) {
+      CK(cudaEventRecord(c->ev_join[k], c->vstream[k]));
+      CK(cudaStreamWaitEvent(s, c->ev_join[k], 0));
     }
   }
   return INPC_OK;
