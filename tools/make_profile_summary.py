@@ -35,7 +35,7 @@ WORKLOAD = {"cfg2": "cfg 2 (2^20 points, 1080p, bilinear, fwd+bwd)",
             "cfg2-env": "cfg 2 with an environment-map background (f2)"}
 lines = [f"# ncu --set full summary ({tag})", "",
          "One launch per kernel, `bench.py --profile-run` (eager, one view), clocks not locked "
-         "(`--clock-control none`).  Units as ncu reports them.  Regenerate: `tools/r01_refresh_ncu.sh` "
+         "(`--clock-control none`).  Units as ncu reports them.  Regenerate: `tools/r02_refresh_ncu.sh` "
          "on the GPU box, then this script.", ""]
 traffic = {}
 for key, rep in reports:
