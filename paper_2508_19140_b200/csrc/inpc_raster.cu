@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are free unless a profiler injects NVTX
+
 #include "inpc_raster.h"
 #include "kernels.cuh"
 #include "single_sort.cuh"
@@ -224,12 +226,20 @@ cudaEvent_t get_event(inpc_ctx* c) {
   return e;
 }
 
+// NVTX range for the lifetime of a scope (API calls, views, stages)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 struct StageTimer {
   inpc_ctx* c;
   cudaStream_t s;
   EventPair ep{};
   bool on;
-  StageTimer(inpc_ctx* ctx, cudaStream_t st, int stage, int launches) : c(ctx), s(st), on(ctx->profiling) {
+  NvtxRange nv;
+  StageTimer(inpc_ctx* ctx, cudaStream_t st, int stage, int launches)
+      : c(ctx), s(st), on(ctx->profiling), nv(kStageNames[stage]) {
     c->stage_launches[stage] += launches;
     if (!on) return;
     c->pending_launches[stage] += launches;
@@ -663,6 +673,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   c->last_stream = s;
   cudaGetLastError();
   AllocScope alloc_scope(c);
+  NvtxRange nv_call("inpc_rasterize_fwd");
 
   DevCam dc;
   DevCfg g;
@@ -1005,6 +1016,7 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   c->last_stream = s;
   cudaGetLastError();
   AllocScope alloc_scope(c);
+  NvtxRange nv_call("inpc_rasterize_bwd");
   const int band_tiles = (g.ty1 - g.ty0) * g.tiles_x;
   const bool gauss = cfg->splat_mode == INPC_SPLAT_GAUSSIAN;
   const int cmax = cmax_for(cfg->C);
