@@ -82,6 +82,10 @@ extern "C" {
                                                     from the camera centre to the point
                                                     (R26); the backward accumulates
                                                     dL/dcoeff into g_point_feat [N,C,9] */
+#define INPC_FLAG_DETERMINISTIC_GRADS (1u << 5) /* backward: no float atomics; every point's
+                                                    per-entry sums added in a fixed order
+                                                    (list position), same bits on every run;
+                                                    syncs once per view, views not overlapped */
 #define INPC_FLAG_ENV_BACKGROUND (1u << 4)       /* NEXT f2: `bg` is an
                                                     equirectangular map [env_h,env_w,C]
                                                     (bg_view_stride 0 or env_h*env_w*C);
@@ -161,7 +165,8 @@ INPC_API int inpc_rasterize_fwd(inpc_ctx* ctx, const inpc_raster_cfg* cfg, const
  *   g_point_feat += dL/df: [N,C] (feat_view_stride 0: summed over views) or
  *                   [V,N,C]; must be 16-byte aligned when C == 4
  *   g_opacity    += dL/do [N] (summed over views)
- * Gradients accumulate with atomics (order of fp32 sums is not fixed). */
+ * Gradients accumulate with atomics (order of fp32 sums is not fixed) unless
+ * cfg.flags has INPC_FLAG_DETERMINISTIC_GRADS. */
 INPC_API int inpc_rasterize_bwd(inpc_ctx* ctx, const inpc_raster_cfg* cfg, const inpc_camera* cams,
                        int32_t V, const float* xyz, const float* feat,
                        int64_t feat_view_stride, const float* opacity, int64_t N,

@@ -28,6 +28,7 @@ FLAG_SKIP_ZERO_ALPHA_GRAD = 1 << 1
 FLAG_DEBUG = 1 << 2
 FLAG_SH_FEATURES = 1 << 3
 FLAG_ENV_BACKGROUND = 1 << 4
+FLAG_DETERMINISTIC_GRADS = 1 << 5
 TILE = 8
 
 EXPORTS = ("inpc_ctx_create", "inpc_ctx_destroy", "inpc_rasterize_fwd", "inpc_rasterize_bwd",

@@ -94,6 +94,7 @@ struct inpc_ctx {
   cudaStream_t vstream[kMaxViewStreams] = {};  // internal non-blocking streams for multi-view calls
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxViewStreams] = {};
   int view_streams = 2;                        // env INPC_VIEW_STREAMS (1 = one stream, A/B)
+  Buf det_f, det_o;  // deterministic gradients: per-entry sums at list positions
   Buf f4_rec, f4_keys, f4_vals, f4_keys2, f4_vals2, f4_hist, f4_scan, f4_misc;  // NEXT f4 baseline
   int bin_grid[3] = {0, 0, 0};  // cooperative grid of k_bin_bilinear<2,4,8>
   bool no_fused_bin = false;     // env INPC_NO_FUSED_BIN=1: separate binning kernels
@@ -194,7 +195,7 @@ void release_all(inpc_ctx* c) {
     for (Buf* b : {&x.chunk_alive, &x.scat, &x.zeroed, &x.cursor, &x.big_tiles, &x.huge_tiles, &x.big_elem,
                    &x.big_chunk, &x.entries, &x.slots, &x.agg, &x.g_eval, &x.tmp, &x.overflow})
       free_buf(*b);
-  for (Buf* b : {&c->f4_rec, &c->f4_keys, &c->f4_vals, &c->f4_keys2, &c->f4_vals2, &c->f4_hist, &c->f4_scan,
+  for (Buf* b : {&c->det_f, &c->det_o, &c->f4_rec, &c->f4_keys, &c->f4_vals, &c->f4_keys2, &c->f4_vals2, &c->f4_hist, &c->f4_scan,
                  &c->f4_misc})
     free_buf(*b);
   for (auto& v : c->views)
@@ -470,6 +471,45 @@ void dispatch_blend_bwd(int cmax, int band_tiles, cudaStream_t s, const DevCam& 
 }
 
 }  // namespace
+
+// Stable LSD radix sort of n (key, value) pairs by the low `bits` key bits
+// on stream s, in the ctx's f4 buffers (keys must already be in f4_keys,
+// values in f4_vals); returns the buffers holding the sorted pairs.
+int radix_pairs(inpc_ctx* c, int64_t n, int bits, cudaStream_t s, unsigned long long** keys_out,
+                uint32_t** vals_out) {
+  const int tiles = (int)((n + kRxTile - 1) / kRxTile);
+  const int64_t hist_n = (int64_t)256 * tiles;
+  const int scan_blocks = (int)((hist_n + kScanTile - 1) / kScanTile);
+  bool fresh = false;
+  int st;
+  if ((st = ensure(c->f4_keys2, (size_t)(n > 0 ? n : 1) * 8, s))) return st;
+  if ((st = ensure(c->f4_vals2, (size_t)(n > 0 ? n : 1) * 4, s))) return st;
+  if ((st = ensure(c->f4_hist, (size_t)(hist_n > 0 ? hist_n : 1) * 4, s))) return st;
+  if ((st = ensure(c->f4_scan, (size_t)scan_blocks * 8 + sizeof(ScanCtl) + 16, s, &fresh))) return st;
+  if (fresh) CK(cudaMemsetAsync(c->f4_scan.p, 0, c->f4_scan.bytes, s));
+  unsigned long long* state = (unsigned long long*)c->f4_scan.p;
+  ScanCtl* ctl = (ScanCtl*)(state + scan_blocks);
+  unsigned long long* ka = (unsigned long long*)c->f4_keys.p;
+  unsigned long long* kb = (unsigned long long*)c->f4_keys2.p;
+  uint32_t* va = (uint32_t*)c->f4_vals.p;
+  uint32_t* vb = (uint32_t*)c->f4_vals2.p;
+  const int rblocks = (tiles + kRxWarps - 1) / kRxWarps;
+  for (int q = 0; n > 0 && q * 8 < bits; ++q) {
+    k_rx_hist<<<rblocks, kRxWarps * 32, 0, s>>>(ka, n, 8 * q, tiles, (uint32_t*)c->f4_hist.p);
+    k_scan_u32<<<scan_blocks, kScanThreads, 0, s>>>(hist_n, (uint32_t*)c->f4_hist.p, state, ctl);
+    k_rx_scatter<<<rblocks, kRxWarps * 32, 0, s>>>(ka, va, n, 8 * q, tiles, (const uint32_t*)c->f4_hist.p, kb, vb);
+    unsigned long long* tk = ka;
+    ka = kb;
+    kb = tk;
+    uint32_t* tv = va;
+    va = vb;
+    vb = tv;
+  }
+  CK(cudaGetLastError());
+  *keys_out = ka;
+  *vals_out = va;
+  return INPC_OK;
+}
 
 extern "C" {
 
@@ -1021,8 +1061,11 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   const bool gauss = cfg->splat_mode == INPC_SPLAT_GAUSSIAN;
   const int cmax = cmax_for(cfg->C);
   const bool packed = !gauss && cfg->C == 4;
-  const int nsets = (V > 1 && !c->profiling) ? (V < c->view_streams ? V : c->view_streams) : 1;
+  const bool det = (cfg->flags & INPC_FLAG_DETERMINISTIC_GRADS) != 0;
+  const int nsets = (V > 1 && !c->profiling && !det) ? (V < c->view_streams ? V : c->view_streams) : 1;
   const bool fork = nsets > 1;
+  int nbits = 1;  // point-index bits for the deterministic reduction's radix passes
+  while (nbits < 32 && ((int64_t)1 << nbits) < N) ++nbits;
   if (sh)
     for (int k = 0; k < nsets; ++k)
       if ((st = ensure(c->scr[k].g_eval, (size_t)N * cfg->C * 4, s))) return st;
@@ -1051,6 +1094,22 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       in.g_feat = (float*)X.g_eval.p;
       if (!packed) feat_v = (const float*)vs.feat_eval.p;
     }
+    in.det_f = nullptr;
+    in.det_o = nullptr;
+    int64_t Ft = 0;
+    if (det) {  // per-entry sums at list positions (F_t read back: deterministic mode syncs once per view)
+      CK(cudaMemcpyAsync(c->host_scalars, vs.scalars.p, sizeof(ViewScalars), cudaMemcpyDeviceToHost, sv));
+      CK(cudaStreamSynchronize(sv));
+      Ft = c->host_scalars[0];
+      if ((st = ensure(c->det_f, (size_t)(Ft > 0 ? Ft : 1) * cfg->C * 4, sv))) return st;
+      if ((st = ensure(c->det_o, (size_t)(Ft > 0 ? Ft : 1) * 4, sv))) return st;
+      if (Ft > 0) {
+        CK(cudaMemsetAsync(c->det_f.p, 0, (size_t)Ft * cfg->C * 4, sv));
+        CK(cudaMemsetAsync(c->det_o.p, 0, (size_t)Ft * 4, sv));
+      }
+      in.det_f = (float*)c->det_f.p;
+      in.det_o = (float*)c->det_o.p;
+    }
     {
       StageTimer tm(c, sv, kStBlendBwd, 1);
       if (gauss)
@@ -1059,6 +1118,20 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       else
         dispatch_blend_bwd<0>(cmax, band_tiles, sv, dc, g, (const PointRec*)vs.rec.p, feat_v, packed, bg_v,
                               (const uint32_t*)vs.ranges.p, (const uint32_t*)vs.sorted_idx.p, in);
+      CK(cudaGetLastError());
+    }
+    if (det && Ft > 0) {  // the fixed-order reduction of the per-entry sums
+      StageTimer tm(c, sv, kStBlendBwd, 3 + 3 * ((nbits + 7) / 8));
+      if ((st = ensure(c->f4_keys, (size_t)Ft * 8, sv))) return st;
+      if ((st = ensure(c->f4_vals, (size_t)Ft * 4, sv))) return st;
+      k_det_keys<<<(unsigned)((Ft + 255) / 256), 256, 0, sv>>>((const uint32_t*)vs.sorted_idx.p, Ft,
+                                                               (unsigned long long*)c->f4_keys.p,
+                                                               (uint32_t*)c->f4_vals.p);
+      unsigned long long* kk = nullptr;
+      uint32_t* vv = nullptr;
+      if ((st = radix_pairs(c, Ft, nbits, sv, &kk, &vv))) return st;
+      k_det_reduce<<<(unsigned)((Ft + 255) / 256), 256, 0, sv>>>(kk, vv, Ft, cfg->C, in.det_f, in.det_o,
+                                                                 in.g_feat, in.g_op);
       CK(cudaGetLastError());
     }
     if (sh) {

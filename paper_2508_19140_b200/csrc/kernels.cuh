@@ -2368,6 +2368,11 @@ struct BwdIn {
   const uint32_t* last;  // saved
   float* g_feat;         // [N,C] +=
   float* g_op;           // [N] +=
+  // deterministic mode (INPC_FLAG_DETERMINISTIC_GRADS): per-entry sums go to
+  // det_f [F_t][C] / det_o [F_t] at the entry's list position (no atomics);
+  // k_det_reduce adds them per point in a fixed order
+  float* det_f;
+  float* det_o;
 };
 
 template <int CMAX>
@@ -2572,7 +2577,17 @@ __global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? 28 / WPB : 1) k_blend_bw
       bool nz = false;
 #pragma unroll
       for (int c = 0; c <= CMAX; ++c) nz |= gsum[c] != 0.0f;
-      if (nz) {
+      if (in.det_o) {  // deterministic mode: this entry's sums at its list position
+        const size_t pos = (size_t)begin + e;
+        if (CMAX == 4 && g.C == 4) {
+          reinterpret_cast<float4*>(in.det_f)[pos] = make_float4(gsum[0], gsum[1], gsum[2], gsum[3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < CMAX; ++c)
+            if (c < g.C) in.det_f[pos * g.C + c] = gsum[c];
+        }
+        in.det_o[pos] = gsum[CMAX];
+      } else if (nz) {
         if (CMAX == 4 && g.C == 4) {
           atomicAdd(reinterpret_cast<float4*>(in.g_feat) + idx,
                     make_float4(gsum[0], gsum[1], gsum[2], gsum[3]));
@@ -2587,6 +2602,41 @@ __global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? 28 / WPB : 1) k_blend_bw
     __syncwarp();
     idx = idx_pf;
   }
+}
+
+// ---------------------------------------------------------------- deterministic gradients
+// INPC_FLAG_DETERMINISTIC_GRADS: the backward writes each entry's sums at its
+// list position; the (point, position) pairs are then stably radix-sorted by
+// point (single_sort.cuh's LSD kernels), so a point's entries follow in
+// ascending list position (tile-major), and k_det_reduce adds them to the
+// point's gradient in that fixed order -- no float atomics, the same bits on
+// every run.
+__global__ void __launch_bounds__(256) k_det_keys(const uint32_t* __restrict__ sorted_idx, int64_t n,
+                                                  unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  keys[k] = sorted_idx[k];
+  vals[k] = (uint32_t)k;
+}
+
+__global__ void __launch_bounds__(256) k_det_reduce(const unsigned long long* __restrict__ keys,
+                                                    const uint32_t* __restrict__ pos, int64_t n, int C,
+                                                    const float* __restrict__ det_f, const float* __restrict__ det_o,
+                                                    float* __restrict__ g_feat, float* __restrict__ g_op) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const uint32_t idx = (uint32_t)keys[k];
+  if (k > 0 && (uint32_t)keys[k - 1] == idx) return;  // the first entry of the point's run sums the run
+  float so = 0.0f;
+  float sf[64];
+  for (int c = 0; c < C; ++c) sf[c] = 0.0f;
+  for (int64_t j = k; j < n && (uint32_t)keys[j] == idx; ++j) {
+    const size_t p = pos[j];
+    for (int c = 0; c < C; ++c) sf[c] += det_f[p * C + c];
+    so += det_o[p];
+  }
+  for (int c = 0; c < C; ++c) g_feat[(size_t)idx * C + c] += sf[c];
+  g_op[idx] += so;
 }
 
 }  // namespace inpc

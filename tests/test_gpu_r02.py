@@ -326,3 +326,40 @@ def test_chunk_culling_changes_nothing(inpc, which):
             np.testing.assert_array_equal(eb["tile_ranges"].cpu().numpy().view(np.uint32), tr)
             np.testing.assert_array_equal(eb["sorted_idx"].cpu().numpy().view(np.uint32), ti)
     a.close(); b.close()
+
+
+@pytest.mark.parametrize("which", ["cfg2", "cfg1_gauss", "cfg1_sh"])
+def test_deterministic_gradients(inpc, ctx, which):
+    """INPC_FLAG_DETERMINISTIC_GRADS: no float atomics in the backward; the
+    gradients are bit-identical across runs and match the oracle."""
+    c = synthgen.config2() if which == "cfg2" else synthgen.config1(seed=61)
+    H, W, C = c["H"], c["W"], c["C"]
+    mode = "gaussian" if which == "cfg1_gauss" else "bilinear"
+    flags = inpc.FLAG_DETERMINISTIC_GRADS
+    feat_np = c["feat"]
+    if which == "cfg1_sh":
+        flags |= inpc.FLAG_SH_FEATURES
+        feat_np = np.random.default_rng(62).normal(0, 0.5, (c["xyz"].shape[0], C, 9)).astype(np.float32)
+    cfg = inpc.make_cfg(H, W, C, mode, flags=flags)
+    xyz, feat, op = dev(c["xyz"]), dev(feat_np), dev(c["opacity"])
+    gF, gA, gD = (dev(x) for x in synthgen.upstream_grads(63, 1, H, W, C))
+    runs = []
+    for _ in range(3):
+        ctx.forward(cfg, c["cams"], xyz, feat, op)
+        gf, go = ctx.backward(cfg, c["cams"], xyz, feat, op, gF, gA, gD)
+        torch.cuda.synchronize()
+        runs.append((gf.cpu().numpy(), go.cpu().numpy()))
+    for r in runs[1:]:
+        assert np.array_equal(r[0].view(np.uint32), runs[0][0].view(np.uint32))
+        assert np.array_equal(r[1].view(np.uint32), runs[0][1].view(np.uint32))
+    if which == "cfg1_sh":
+        f_or, Y = oracle.sh_features(c["cams"][0], c["xyz"], feat_np)
+        o = oracle.backward(c["cams"][0], c["xyz"], f_or, c["opacity"], H, W,
+                            *(x[0].cpu().numpy() for x in (gF, gA, gD)))
+        check_grads(runs[0][0], o["g_feat"][:, :, None] * Y[:, None, :])
+    else:
+        kw = dict(mode="gaussian", sigma=0.0) if mode == "gaussian" else {}
+        o = oracle.backward(c["cams"][0], c["xyz"], c["feat"], c["opacity"], H, W,
+                            *(x[0].cpu().numpy() for x in (gF, gA, gD)), threads=oracle.max_threads(), **kw)
+        check_grads(runs[0][0], o["g_feat"])
+    check_grads(runs[0][1], o["g_opacity"])
