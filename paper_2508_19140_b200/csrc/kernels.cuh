@@ -1735,6 +1735,250 @@ __global__ void __launch_bounds__(kMidThreads) k_sort_mid(const uint32_t* __rest
   }
 }
 
+// ---------------------------------------------------------------- H4+H6 (mid tiles, merge sort)
+// NT threads per tile of LO < n <= MAXN entries, grid-stride over the
+// big-tile list.  The tile's keys become unique 32-bit keys (depth - tile
+// minimum, quantised to 32 - SB bits) << SB | list slot; each thread sorts a
+// run of q = (padded n) / NT keys in registers (sorting network, no
+// shuffles), then log2(NT) merge passes through SMEM ping-pong buffers:
+// thread t writes outputs [t q, (t + 1) q) of every pass, starting from a
+// merge-path co-rank search, so an output costs a handful of instructions
+// instead of a network stage or a radix pass per key.  Quantisation ties are
+// put in (depth, index) order on the full keys (short runs: insertion; long
+// runs: 64-bit bitonic of the whole tile in the same SMEM).  Same lists, bit
+// for bit, as every other sort path (R7/R8).  NT > 32 spreads one tile's
+// serial merge chain over more threads (a warp per 2k-entry tile is bound by
+// the latency of its ~400 dependent merge steps).
+template <int NT, int MAXN>
+struct MidMerge {
+  static constexpr int kSlotBits = MAXN == 1024 ? 10 : 11;
+  static constexpr int kPad = MAXN + MAXN / 32;  // one spare word per 32: conflict-free thread strides
+  static constexpr int kMaxRun = 64;
+  static constexpr int kQMax = MAXN / NT;
+  static constexpr size_t kSmem = 2 * (size_t)kPad * 4;
+  static_assert(MAXN == (1 << kSlotBits), "slot bits");
+  static_assert(kQMax >= 4 && kQMax <= 32, "run length");
+};
+
+__device__ __forceinline__ int mw_phys(int x) { return x + (x >> 5); }
+
+template <int NT>
+__device__ __forceinline__ void mm_sync() {
+  if (NT == 32) __syncwarp();
+  else __syncthreads();
+}
+
+// Sorting network on Q keys in registers (compile-time indices): ascending.
+template <int Q>
+__device__ __forceinline__ void lane_sort(uint32_t (&v)[Q]) {
+#pragma unroll
+  for (int k = 2; k <= Q; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint32_t a = v[i], b = v[l];
+          if ((i & k) == 0) {
+            v[i] = min(a, b);
+            v[l] = max(a, b);
+          } else {
+            v[i] = max(a, b);
+            v[l] = min(a, b);
+          }
+        }
+      }
+}
+
+// Run `run` of R0 keys (from the quantised depths in db) sorted in registers,
+// stored to dst.
+template <int R0>
+__device__ __forceinline__ void mm_run(const uint32_t* db, uint32_t* dst, int run, int n, uint32_t dmin,
+                                       int shift, int sb) {
+  uint32_t v[R0];
+  const int s = run * R0;
+#pragma unroll
+  for (int t = 0; t < R0; ++t) {
+    const int i = s + t;
+    v[t] = i < n ? (((db[mw_phys(i)] - dmin) >> shift) << sb) | (uint32_t)i : 0xFFFFFFFFu;
+  }
+  lane_sort<R0>(v);
+#pragma unroll
+  for (int t = 0; t < R0; ++t) dst[mw_phys(s + t)] = v[t];
+}
+
+// Ascending bitonic sort of np (power of two) 64-bit keys in SMEM by NT threads.
+template <int NT>
+__device__ __forceinline__ void mm_bitonic64(unsigned long long* s, int np, int tid) {
+  for (int k = 2; k <= np; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = tid; t < (np >> 1); t += NT) {
+        const int i = 2 * t - (t & (j - 1));
+        const int ixj = i + j;
+        const unsigned long long a = s[i], b = s[ixj];
+        const bool up = (i & k) == 0;
+        if ((a > b) == up) {
+          s[i] = b;
+          s[ixj] = a;
+        }
+      }
+      mm_sync<NT>();
+    }
+}
+
+template <int NT, int MAXN>
+__global__ void __launch_bounds__(NT) k_sort_mid_merge(
+    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles, ViewScalars* __restrict__ sc,
+    const unsigned long long* __restrict__ entries, uint32_t* __restrict__ sorted_idx, uint32_t lo_n,
+    uint32_t* __restrict__ done) {
+  using M = MidMerge<NT, MAXN>;
+  constexpr int NW = NT / 32;
+  __shared__ __align__(16) uint32_t buf[2 * M::kPad];
+  __shared__ uint32_t red[2][NW];
+  __shared__ uint32_t s_last;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t* buf0 = buf;
+  uint32_t* buf1 = buf + M::kPad;
+  constexpr int SB = M::kSlotBits;
+  constexpr uint32_t smask = (uint32_t)MAXN - 1u;
+  const uint32_t nb = sc->num_big;
+  for (uint32_t j = blockIdx.x; j < nb; j += gridDim.x) {
+    const uint32_t t = big_tiles[j];
+    const uint32_t begin = ranges[t], n = ranges[t + 1] - begin;
+    if (n <= lo_n || n > (uint32_t)MAXN) continue;  // block-uniform
+    const unsigned long long* src = entries + begin;
+    // depth bits to buf1 (logical layout), tile minimum / maximum
+    uint32_t dlo = 0xFFFFFFFFu, dhi = 0u;
+    for (uint32_t i = tid; i < n; i += NT) {
+      const uint32_t d = (uint32_t)(__ldg(src + i) >> 32);
+      buf1[mw_phys((int)i)] = d;
+      dlo = min(dlo, d);
+      dhi = max(dhi, d);
+    }
+    dlo = __reduce_min_sync(0xffffffffu, dlo);
+    dhi = __reduce_max_sync(0xffffffffu, dhi);
+    if (NW > 1) {
+      if (lane == 0) {
+        red[0][w] = dlo;
+        red[1][w] = dhi;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < NW; ++k) {
+        dlo = min(dlo, red[0][k]);
+        dhi = max(dhi, red[1][k]);
+      }
+    } else {
+      __syncwarp();
+    }
+    const uint32_t range = dhi - dlo;
+    const int vbits = range ? 32 - __clz(range) : 0;
+    const int shift = vbits > 32 - SB ? vbits - (32 - SB) : 0;
+    // per-thread runs of q keys sorted in registers, written to buf0
+    int q = M::kQMax;
+    while (q > 4 && (uint32_t)(q >> 1) * NT >= n) q >>= 1;
+    if (q == M::kQMax) mm_run<M::kQMax>(buf1, buf0, tid, (int)n, dlo, shift, SB);
+    else if (M::kQMax >= 8 && q == M::kQMax / 2) mm_run<(M::kQMax >= 8 ? M::kQMax / 2 : 4)>(buf1, buf0, tid, (int)n, dlo, shift, SB);
+    else mm_run<4>(buf1, buf0, tid, (int)n, dlo, shift, SB);
+    mm_sync<NT>();
+    // merge passes: runs of L -> 2L; thread t writes outputs [t q, t q + q)
+    const int np = NT * q;
+    uint32_t* srcb = buf0;
+    uint32_t* dstb = buf1;
+    for (int L = q; L < np; L <<= 1) {
+      const int o0 = tid * q;
+      const int P = o0 & ~(2 * L - 1);
+      const int d = o0 - P;
+      int lo = d > L ? d - L : 0, hi = d < L ? d : L;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (srcb[mw_phys(P + mid)] <= srcb[mw_phys(P + L + d - mid - 1)]) lo = mid + 1;
+        else hi = mid;
+      }
+      int ia = lo, ib = d - lo;
+      uint32_t a = ia < L ? srcb[mw_phys(P + ia)] : 0xFFFFFFFFu;
+      uint32_t b = ib < L ? srcb[mw_phys(P + L + ib)] : 0xFFFFFFFFu;
+      // branch-free: one select of the taken side, one load of its successor
+      uint32_t* dp = dstb + mw_phys(o0);  // q <= 32 outputs of one thread stay in one 32-word row
+#pragma unroll 4
+      for (int k = 0; k < q; ++k) {
+        const bool ta = a <= b;
+        dp[k] = ta ? a : b;
+        ia += ta;
+        ib += !ta;
+        const int nx = ta ? ia : L + ib;
+        const uint32_t v = (ta ? ia : ib) < L ? srcb[mw_phys(P + nx)] : 0xFFFFFFFFu;
+        a = ta ? v : a;
+        b = ta ? b : v;
+      }
+      mm_sync<NT>();
+      uint32_t* tmp = srcb;
+      srcb = dstb;
+      dstb = tmp;
+    }
+    // equal quantised depths: (depth, index) order on the full keys
+    bool tie_bad = false;
+    for (uint32_t p = tid; p + 1 < n; p += NT) {
+      const uint32_t ka = srcb[mw_phys((int)p)], kb = srcb[mw_phys((int)p + 1)];
+      if ((ka >> SB) == (kb >> SB) && __ldg(src + (ka & smask)) > __ldg(src + (kb & smask))) tie_bad = true;
+    }
+    const bool any_bad = NT == 32 ? __any_sync(0xffffffffu, tie_bad) : __syncthreads_or(tie_bad);
+    if (any_bad) {
+      bool too_long = false;
+      for (uint32_t p = tid; p + 1 < n; p += NT) {
+        const uint32_t a0 = srcb[mw_phys((int)p)] >> SB;
+        if ((srcb[mw_phys((int)p + 1)] >> SB) != a0 || (p > 0 && (srcb[mw_phys((int)p - 1)] >> SB) == a0)) continue;
+        uint32_t end = p + 2;
+        while (end < n && (srcb[mw_phys((int)end)] >> SB) == a0 && end - p <= (uint32_t)M::kMaxRun) ++end;
+        if (end - p > (uint32_t)M::kMaxRun) {
+          too_long = true;
+          continue;
+        }
+        for (uint32_t k = p + 1; k < end; ++k) {  // insertion sort of the run on the full keys
+          const uint32_t v = srcb[mw_phys((int)k)];
+          const unsigned long long fv = __ldg(src + (v & smask));
+          int jj = (int)k - 1;
+          while (jj >= (int)p && __ldg(src + (srcb[mw_phys(jj)] & smask)) > fv) {
+            srcb[mw_phys(jj + 1)] = srcb[mw_phys(jj)];
+            --jj;
+          }
+          srcb[mw_phys(jj + 1)] = v;
+        }
+      }
+      if (NT == 32) __syncwarp();
+      const bool any_long = NT == 32 ? __any_sync(0xffffffffu, too_long) : __syncthreads_or(too_long);
+      if (any_long) {  // long tie runs: 64-bit bitonic of the tile
+        unsigned long long* s64 = reinterpret_cast<unsigned long long*>(buf);
+        int np2 = 32;
+        while (np2 < (int)n) np2 <<= 1;
+        for (int i = tid; i < np2; i += NT) s64[i] = i < (int)n ? __ldg(src + i) : ~0ull;
+        mm_sync<NT>();
+        mm_bitonic64<NT>(s64, np2, tid);
+        for (uint32_t i = tid; i < n; i += NT) sorted_idx[begin + i] = (uint32_t)s64[i];
+        mm_sync<NT>();
+        continue;
+      }
+    }
+    const uint32_t* src32 = reinterpret_cast<const uint32_t*>(src);  // low word = point index
+    for (uint32_t i = tid; i < n; i += NT) sorted_idx[begin + i] = __ldg(src32 + 2 * (srcb[mw_phys((int)i)] & smask));
+    mm_sync<NT>();
+  }
+  if (!done) return;
+  // the last CTA of the last mid kernel clears the list count for the next call
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    *done = 0u;
+    sc->num_big = 0u;
+    sc->max_big = 0u;
+  }
+}
+
 // ---------------------------------------------------------------- H1..H6 fused (bilinear)
 // One cooperative launch for the whole binning of a bilinear view: every
 // thread keeps KP points' depth key, tile block and entry slots in

@@ -309,7 +309,10 @@ def test_unfused_binning_cfg2(inpc, ctx_unfused):
 
 @pytest.mark.parametrize("n,ties", [(5000, "long"), (6000, "short"), (6000, "none"), (3000, "short"),
                                     (20000, "short"), (2100, "none"), (1500, "short"), (1500, "long"),
-                                    (300, "none"), (2048, "short")])
+                                    (300, "none"), (2048, "short"),
+                                    # warp merge sort of the mid tiles (257..1024, 1025..2048)
+                                    (257, "none"), (513, "short"), (600, "short"), (700, "long"),
+                                    (1000, "none"), (1024, "short"), (1025, "long"), (1800, "none")])
 def test_unfused_big_tile(inpc, ctx_unfused, n, ties):
     """k_sort_big: radix chunks (> 2048 entries) with short tie runs fixed up
     in index order, 32-bit-key bitonic chunks (<= 2048) with odd-even
