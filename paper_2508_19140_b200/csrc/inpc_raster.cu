@@ -101,6 +101,8 @@ struct inpc_ctx {
   Buf f4_rec, f4_keys, f4_vals, f4_keys2, f4_vals2, f4_hist, f4_scan, f4_misc;  // NEXT f4 baseline
   int bin_grid[3] = {0, 0, 0};  // cooperative grid of k_bin_bilinear<2,4,8>
   bool no_fused_bin = false;     // env INPC_NO_FUSED_BIN=1: separate binning kernels
+  bool rec16_pref = true;        // env INPC_REC16=0: 32-byte records with packed features (A/B)
+  bool rec16 = false;            // saved state: the forward wrote 16-byte records
   uint64_t entry_cap = 0;
   std::vector<ViewState> views;
   // saved-state signature
@@ -587,6 +589,8 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
   {
     const char* e = getenv("INPC_NO_FUSED_BIN");
     c->no_fused_bin = e && e[0] == '1';
+    const char* r = getenv("INPC_REC16");
+    c->rec16_pref = !(r && r[0] == '0');
   }
   {
     const char* e = getenv("INPC_VIEW_STREAMS");
@@ -738,7 +742,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   const bool gauss = cfg->splat_mode == INPC_SPLAT_GAUSSIAN;
   const bool debug = (cfg->flags & INPC_FLAG_DEBUG) != 0;
   const int cmax = cmax_for(cfg->C);
-  const bool packed = !gauss && cfg->C == 4;  // features travel in the point record
+  bool packed = !gauss && cfg->C == 4;  // features travel in the point record (unless rec16)
 
   // scratch
   const int scan_blocks = (T + kScanTile - 1) / kScanTile;
@@ -765,6 +769,10 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
         break;
       }
   }
+  // unfused bilinear binning: 16-byte records {u, v, z, o}, the blends read
+  // the features from feat (measured on cfg 5: see DESIGN.md)
+  const bool rec16 = c->rec16_pref && !gauss && !sh && !debug && !fused_kp && N > 0 && T < (1 << 28);
+  if (rec16) packed = false;
   // entry capacity per view: bilinear 4N; Gaussian a static bound when it
   // fits a quarter of the free memory (sync-free), else F_t read back per view
   std::vector<uint64_t> need_v(V, bound);
@@ -840,6 +848,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
 
   for (int v = 0; v < V; ++v) {
     make_dev(cfg, cams[v], dc, g);
+    if (rec16) g.flags |= kFlagRec16;
     ViewState& vs = c->views[v];
     Scratch& X = c->scr[v % nsets];
     const cudaStream_t sv = fork ? c->vstream[v % nsets] : s;
@@ -1032,6 +1041,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     }
   }
   c->have_state = true;
+  c->rec16 = rec16;
   c->V = V;
   c->N = N;
   c->H = cfg->H;
@@ -1091,7 +1101,7 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   const int band_tiles = (g.ty1 - g.ty0) * g.tiles_x;
   const bool gauss = cfg->splat_mode == INPC_SPLAT_GAUSSIAN;
   const int cmax = cmax_for(cfg->C);
-  const bool packed = !gauss && cfg->C == 4;
+  const bool packed = !gauss && cfg->C == 4 && !c->rec16;  // the forward's record layout
   const bool det = (cfg->flags & INPC_FLAG_DETERMINISTIC_GRADS) != 0;
   const int nsets = (V > 1 && !c->profiling && !det) ? (V < c->view_streams ? V : c->view_streams) : 1;
   const bool fork = nsets > 1;
@@ -1106,6 +1116,7 @@ int inpc_rasterize_bwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   }
   for (int v = 0; v < V; ++v) {
     make_dev(cfg, cams[v], dc, g);
+    if (c->rec16) g.flags |= kFlagRec16;
     ViewState& vs = c->views[v];
     Scratch& X = c->scr[v % nsets];
     const cudaStream_t sv = fork ? c->vstream[v % nsets] : s;

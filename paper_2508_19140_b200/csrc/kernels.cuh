@@ -325,10 +325,14 @@ __global__ void __launch_bounds__(kPointThreads, 4) k_project_count(
           base[c] = atomicAdd(tile_count + tile[c], (uint32_t)__popc(peers[c]));
       }
       if (ok) {
-        PointRec pr;
-        pr.a = make_float4(p.u, p.v, p.zc, O[k]);
-        pr.b = pack ? Fv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
-        rec[i] = pr;
+        if (g.flags & kFlagRec16) {  // compact record, features stay in feat
+          reinterpret_cast<float4*>(rec)[i] = make_float4(p.u, p.v, p.zc, O[k]);
+        } else {
+          PointRec pr;
+          pr.a = make_float4(p.u, p.v, p.zc, O[k]);
+          pr.b = pack ? Fv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+          rec[i] = pr;
+        }
       }
       uint32_t sl[4];
 #pragma unroll
@@ -2283,8 +2287,13 @@ __device__ __forceinline__ EntryRegs load_entry(const DevCfg& g, const PointRec*
                                                 uint32_t idx) {
   EntryRegs r;
   r.idx = idx;
-  r.A = __ldg(&rec[idx].a);
-  r.B = __ldg(&rec[idx].b);
+  if (g.flags & kFlagRec16) {
+    r.A = __ldg(reinterpret_cast<const float4*>(rec) + idx);
+    r.B = make_float4(0.f, 0.f, 0.f, 0.f);
+  } else {
+    r.A = __ldg(&rec[idx].a);
+    r.B = __ldg(&rec[idx].b);
+  }
   if (CMAX == 4 && !packed && g.C == 4) r.F = __ldg(reinterpret_cast<const float4*>(feat) + idx);
   return r;
 }
@@ -2301,8 +2310,12 @@ __device__ __forceinline__ void prefetch_entry(RB& rb, const DevCfg& g, const Po
                                                const float* __restrict__ feat, bool packed, uint32_t idx,
                                                bool valid, int lane) {
   if (valid) {
-    cp_async16(&rb.A[lane], &rec[idx].a);
-    cp_async16(&rb.B[lane], &rec[idx].b);
+    if (g.flags & kFlagRec16) {
+      cp_async16(&rb.A[lane], reinterpret_cast<const float4*>(rec) + idx);
+    } else {
+      cp_async16(&rb.A[lane], &rec[idx].a);
+      cp_async16(&rb.B[lane], &rec[idx].b);
+    }
     if (CMAX == 4 && !packed && g.C == 4) cp_async16(&rb.F[lane], reinterpret_cast<const float4*>(feat) + idx);
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -2537,7 +2550,13 @@ __device__ __forceinline__ void write_pixel(const DevCam& cam, const DevCfg& g, 
 // lists ended by early termination) 514 -> 780 us, so dense clouds run
 // without).
 template <int MODE, int CMAX, bool COUNT, int WPB = kWarpsPerBlock, bool PF = false>
-__global__ void __launch_bounds__(WPB * 32) k_blend_fwd(
+#ifndef INPC_FWD_MINB
+#define INPC_FWD_MINB 8  // 64 registers (measured optimum: 76 at 1, 48 + spills at 10 are slower)
+#endif
+#ifndef INPC_BWD_WARPS_PER_SM
+#define INPC_BWD_WARPS_PER_SM 28
+#endif
+__global__ void __launch_bounds__(WPB * 32, INPC_FWD_MINB) k_blend_fwd(
     DevCam cam, DevCfg g, int band_tiles, const PointRec* __restrict__ rec,
     const float* __restrict__ feat, bool packed, const float* __restrict__ bg,
     const uint32_t* __restrict__ ranges, const unsigned long long* __restrict__ entries,
@@ -2744,7 +2763,7 @@ __device__ __forceinline__ uint32_t below_mask(uint32_t last, uint32_t base) {
 
 // 7 CTAs of 4 warps per SM (<= 73 registers): measured 82 vs 93 us at 6 CTAs on cfg 2
 template <int MODE, int CMAX, int WPB = kWarpsPerBlock>
-__global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? 28 / WPB : 1) k_blend_bwd(
+__global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? INPC_BWD_WARPS_PER_SM / WPB : 1) k_blend_bwd(
     DevCam cam, DevCfg g, int band_tiles, const PointRec* __restrict__ rec,
     const float* __restrict__ feat, bool packed, const float* __restrict__ bg,
     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ sorted_idx, BwdIn in) {

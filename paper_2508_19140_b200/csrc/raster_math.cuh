@@ -30,6 +30,7 @@ constexpr unsigned kFlagSigmaPx = 1u;
 constexpr unsigned kFlagSkipZero = 2u;
 constexpr unsigned kFlagSH = 4u;
 constexpr unsigned kFlagEnv = 8u;
+constexpr unsigned kFlagRec16 = 1u << 29;  // internal: bilinear records are 16-byte {u, v, z, o}, features read from feat
 
 struct Proj {
   float xc, yc, zc, u, v, xz, yz;
