@@ -86,7 +86,6 @@ struct inpc_ctx {
   bool no_mid_sort = false; // env INPC_NO_MID_SORT=1: every big tile through k_sort_big (A/B)
   bool mid_cta = false;     // env INPC_MID_SORT=cta: mid tiles through the CTA radix k_sort_mid (A/B)
   int midw_grid[2] = {0, 0}; // k_sort_mid_merge (<= 1024, <= 2048 entries): resident CTAs
-  int mid_nt1 = 64;          // env INPC_MID_NT1: threads per tile of <= 1024 entries (32 / 64 / 128)
   // chunk bounds of a static cloud (inpc_ctx_set_chunks): used by forwards over that cloud
   const float* chunk_box = nullptr;
   const float* chunk_xyz = nullptr;
@@ -563,13 +562,8 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
     c->no_mid_sort = e && e[0] == '1';
     const char* m = getenv("INPC_MID_SORT");
     c->mid_cta = m && !strcmp(m, "cta");
-    const char* m1 = getenv("INPC_MID_NT1");
-    c->mid_nt1 = m1 ? atoi(m1) : 64;
-    if (c->mid_nt1 != 32 && c->mid_nt1 != 64 && c->mid_nt1 != 128) c->mid_nt1 = 64;
     int o1 = 0, o2 = 0;
-    if (c->mid_nt1 == 32) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_sort_mid_merge<32, 1024>, 32, 0);
-    else if (c->mid_nt1 == 64) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_sort_mid_merge<64, 1024>, 64, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_sort_mid_merge<128, 1024>, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_sort_mid_merge<64, 1024>, 64, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_sort_mid_merge<128, 2048>, 128, 0);
     c->midw_grid[0] = c->num_sms * (o1 > 0 ? o1 : 1);
     c->midw_grid[1] = c->num_sms * (o2 > 0 ? o2 : 1);
@@ -972,12 +966,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
         const uint32_t* bp = (const uint32_t*)X.big_tiles.p;
         const unsigned long long* ep = (const unsigned long long*)X.entries.p;
         uint32_t* sp = (uint32_t*)vs.sorted_idx.p;
-        if (c->mid_nt1 == 32)
-          k_sort_mid_merge<32, 1024><<<c->midw_grid[0], 32, 0, sv>>>(rp, bp, sc, ep, sp, (uint32_t)kWarpSortCap, nullptr);
-        else if (c->mid_nt1 == 64)
-          k_sort_mid_merge<64, 1024><<<c->midw_grid[0], 64, 0, sv>>>(rp, bp, sc, ep, sp, (uint32_t)kWarpSortCap, nullptr);
-        else
-          k_sort_mid_merge<128, 1024><<<c->midw_grid[0], 128, 0, sv>>>(rp, bp, sc, ep, sp, (uint32_t)kWarpSortCap, nullptr);
+        k_sort_mid_merge<64, 1024><<<c->midw_grid[0], 64, 0, sv>>>(rp, bp, sc, ep, sp, (uint32_t)kWarpSortCap, nullptr);
         CK(cudaGetLastError());
         k_sort_mid_merge<128, 2048><<<c->midw_grid[1], 128, 0, sv>>>(rp, bp, sc, ep, sp, 1024u,
                                                                       (uint32_t*)X.overflow.p + 6);

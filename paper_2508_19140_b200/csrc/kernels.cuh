@@ -1756,15 +1756,12 @@ __global__ void __launch_bounds__(kMidThreads) k_sort_mid(const uint32_t* __rest
 template <int NT, int MAXN>
 struct MidMerge {
   static constexpr int kSlotBits = MAXN == 1024 ? 10 : 11;
-  static constexpr int kPad = MAXN + MAXN / 32;  // one spare word per 32: conflict-free thread strides
+  static constexpr int kQMax = MAXN / NT + 1;     // keys per thread (odd: conflict-free thread strides)
+  static constexpr int kBuf = NT * kQMax;         // padded tile length
   static constexpr int kMaxRun = 64;
-  static constexpr int kQMax = MAXN / NT;
-  static constexpr size_t kSmem = 2 * (size_t)kPad * 4;
   static_assert(MAXN == (1 << kSlotBits), "slot bits");
-  static_assert(kQMax >= 4 && kQMax <= 32, "run length");
+  static_assert(kQMax <= 17 && 2 * kBuf * 4 >= MAXN * 8, "run length / 64-bit fallback room");
 };
-
-__device__ __forceinline__ int mw_phys(int x) { return x + (x >> 5); }
 
 template <int NT>
 __device__ __forceinline__ void mm_sync() {
@@ -1795,21 +1792,23 @@ __device__ __forceinline__ void lane_sort(uint32_t (&v)[Q]) {
       }
 }
 
-// Run `run` of R0 keys (from the quantised depths in db) sorted in registers,
-// stored to dst.
-template <int R0>
-__device__ __forceinline__ void mm_run(const uint32_t* db, uint32_t* dst, int run, int n, uint32_t dmin,
+// Run `run` (keys [run q, run q + q), from the quantised depths in db) sorted
+// in a Q-register network (Q >= q, the extra registers hold the pad key),
+// its q smallest stored to dst.
+template <int Q>
+__device__ __forceinline__ void mm_run(const uint32_t* db, uint32_t* dst, int run, int q, int n, uint32_t dmin,
                                        int shift, int sb) {
-  uint32_t v[R0];
-  const int s = run * R0;
+  uint32_t v[Q];
+  const int s = run * q;
 #pragma unroll
-  for (int t = 0; t < R0; ++t) {
+  for (int t = 0; t < Q; ++t) {
     const int i = s + t;
-    v[t] = i < n ? (((db[mw_phys(i)] - dmin) >> shift) << sb) | (uint32_t)i : 0xFFFFFFFFu;
+    v[t] = (t < q && i < n) ? (((db[i] - dmin) >> shift) << sb) | (uint32_t)i : 0xFFFFFFFFu;
   }
-  lane_sort<R0>(v);
+  lane_sort<Q>(v);
 #pragma unroll
-  for (int t = 0; t < R0; ++t) dst[mw_phys(s + t)] = v[t];
+  for (int t = 0; t < Q; ++t)
+    if (t < q) dst[s + t] = v[t];
 }
 
 // Ascending bitonic sort of np (power of two) 64-bit keys in SMEM by NT threads.
@@ -1838,12 +1837,12 @@ __global__ void __launch_bounds__(NT) k_sort_mid_merge(
     uint32_t* __restrict__ done) {
   using M = MidMerge<NT, MAXN>;
   constexpr int NW = NT / 32;
-  __shared__ __align__(16) uint32_t buf[2 * M::kPad];
+  __shared__ __align__(16) uint32_t buf[2 * M::kBuf];
   __shared__ uint32_t red[2][NW];
   __shared__ uint32_t s_last;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   uint32_t* buf0 = buf;
-  uint32_t* buf1 = buf + M::kPad;
+  uint32_t* buf1 = buf + M::kBuf;
   constexpr int SB = M::kSlotBits;
   constexpr uint32_t smask = (uint32_t)MAXN - 1u;
   const uint32_t nb = sc->num_big;
@@ -1852,11 +1851,11 @@ __global__ void __launch_bounds__(NT) k_sort_mid_merge(
     const uint32_t begin = ranges[t], n = ranges[t + 1] - begin;
     if (n <= lo_n || n > (uint32_t)MAXN) continue;  // block-uniform
     const unsigned long long* src = entries + begin;
-    // depth bits to buf1 (logical layout), tile minimum / maximum
+    // depth bits to buf1, tile minimum / maximum
     uint32_t dlo = 0xFFFFFFFFu, dhi = 0u;
     for (uint32_t i = tid; i < n; i += NT) {
       const uint32_t d = (uint32_t)(__ldg(src + i) >> 32);
-      buf1[mw_phys((int)i)] = d;
+      buf1[i] = d;
       dlo = min(dlo, d);
       dhi = max(dhi, d);
     }
@@ -1879,12 +1878,12 @@ __global__ void __launch_bounds__(NT) k_sort_mid_merge(
     const uint32_t range = dhi - dlo;
     const int vbits = range ? 32 - __clz(range) : 0;
     const int shift = vbits > 32 - SB ? vbits - (32 - SB) : 0;
-    // per-thread runs of q keys sorted in registers, written to buf0
-    int q = M::kQMax;
-    while (q > 4 && (uint32_t)(q >> 1) * NT >= n) q >>= 1;
-    if (q == M::kQMax) mm_run<M::kQMax>(buf1, buf0, tid, (int)n, dlo, shift, SB);
-    else if (M::kQMax >= 8 && q == M::kQMax / 2) mm_run<(M::kQMax >= 8 ? M::kQMax / 2 : 4)>(buf1, buf0, tid, (int)n, dlo, shift, SB);
-    else mm_run<4>(buf1, buf0, tid, (int)n, dlo, shift, SB);
+    // per-thread runs of q keys (q odd: the thread strides of every pass hit
+    // distinct banks) sorted in registers, written to buf0
+    const int q = (((int)n + NT - 1) / NT) | 1;
+    if (q <= 8) mm_run<8>(buf1, buf0, tid, q, (int)n, dlo, shift, SB);
+    else if (q <= 16) mm_run<16>(buf1, buf0, tid, q, (int)n, dlo, shift, SB);
+    else mm_run<32>(buf1, buf0, tid, q, (int)n, dlo, shift, SB);
     mm_sync<NT>();
     // merge passes: runs of L -> 2L; thread t writes outputs [t q, t q + q)
     const int np = NT * q;
@@ -1892,19 +1891,19 @@ __global__ void __launch_bounds__(NT) k_sort_mid_merge(
     uint32_t* dstb = buf1;
     for (int L = q; L < np; L <<= 1) {
       const int o0 = tid * q;
-      const int P = o0 & ~(2 * L - 1);
+      const int P = o0 / (2 * L) * (2 * L);  // 2L = q 2^(p+1), q odd
       const int d = o0 - P;
       int lo = d > L ? d - L : 0, hi = d < L ? d : L;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (srcb[mw_phys(P + mid)] <= srcb[mw_phys(P + L + d - mid - 1)]) lo = mid + 1;
+        if (srcb[P + mid] <= srcb[P + L + d - mid - 1]) lo = mid + 1;
         else hi = mid;
       }
       int ia = lo, ib = d - lo;
-      uint32_t a = ia < L ? srcb[mw_phys(P + ia)] : 0xFFFFFFFFu;
-      uint32_t b = ib < L ? srcb[mw_phys(P + L + ib)] : 0xFFFFFFFFu;
+      uint32_t a = ia < L ? srcb[P + ia] : 0xFFFFFFFFu;
+      uint32_t b = ib < L ? srcb[P + L + ib] : 0xFFFFFFFFu;
       // branch-free: one select of the taken side, one load of its successor
-      uint32_t* dp = dstb + mw_phys(o0);  // q <= 32 outputs of one thread stay in one 32-word row
+      uint32_t* dp = dstb + o0;
 #pragma unroll 4
       for (int k = 0; k < q; ++k) {
         const bool ta = a <= b;
@@ -1912,7 +1911,7 @@ __global__ void __launch_bounds__(NT) k_sort_mid_merge(
         ia += ta;
         ib += !ta;
         const int nx = ta ? ia : L + ib;
-        const uint32_t v = (ta ? ia : ib) < L ? srcb[mw_phys(P + nx)] : 0xFFFFFFFFu;
+        const uint32_t v = (ta ? ia : ib) < L ? srcb[P + nx] : 0xFFFFFFFFu;
         a = ta ? v : a;
         b = ta ? b : v;
       }
@@ -1924,30 +1923,30 @@ __global__ void __launch_bounds__(NT) k_sort_mid_merge(
     // equal quantised depths: (depth, index) order on the full keys
     bool tie_bad = false;
     for (uint32_t p = tid; p + 1 < n; p += NT) {
-      const uint32_t ka = srcb[mw_phys((int)p)], kb = srcb[mw_phys((int)p + 1)];
+      const uint32_t ka = srcb[p], kb = srcb[p + 1];
       if ((ka >> SB) == (kb >> SB) && __ldg(src + (ka & smask)) > __ldg(src + (kb & smask))) tie_bad = true;
     }
     const bool any_bad = NT == 32 ? __any_sync(0xffffffffu, tie_bad) : __syncthreads_or(tie_bad);
     if (any_bad) {
       bool too_long = false;
       for (uint32_t p = tid; p + 1 < n; p += NT) {
-        const uint32_t a0 = srcb[mw_phys((int)p)] >> SB;
-        if ((srcb[mw_phys((int)p + 1)] >> SB) != a0 || (p > 0 && (srcb[mw_phys((int)p - 1)] >> SB) == a0)) continue;
+        const uint32_t a0 = srcb[p] >> SB;
+        if ((srcb[p + 1] >> SB) != a0 || (p > 0 && (srcb[p - 1] >> SB) == a0)) continue;
         uint32_t end = p + 2;
-        while (end < n && (srcb[mw_phys((int)end)] >> SB) == a0 && end - p <= (uint32_t)M::kMaxRun) ++end;
+        while (end < n && (srcb[end] >> SB) == a0 && end - p <= (uint32_t)M::kMaxRun) ++end;
         if (end - p > (uint32_t)M::kMaxRun) {
           too_long = true;
           continue;
         }
         for (uint32_t k = p + 1; k < end; ++k) {  // insertion sort of the run on the full keys
-          const uint32_t v = srcb[mw_phys((int)k)];
+          const uint32_t v = srcb[k];
           const unsigned long long fv = __ldg(src + (v & smask));
           int jj = (int)k - 1;
-          while (jj >= (int)p && __ldg(src + (srcb[mw_phys(jj)] & smask)) > fv) {
-            srcb[mw_phys(jj + 1)] = srcb[mw_phys(jj)];
+          while (jj >= (int)p && __ldg(src + (srcb[jj] & smask)) > fv) {
+            srcb[jj + 1] = srcb[jj];
             --jj;
           }
-          srcb[mw_phys(jj + 1)] = v;
+          srcb[jj + 1] = v;
         }
       }
       if (NT == 32) __syncwarp();
@@ -1965,7 +1964,7 @@ __global__ void __launch_bounds__(NT) k_sort_mid_merge(
       }
     }
     const uint32_t* src32 = reinterpret_cast<const uint32_t*>(src);  // low word = point index
-    for (uint32_t i = tid; i < n; i += NT) sorted_idx[begin + i] = __ldg(src32 + 2 * (srcb[mw_phys((int)i)] & smask));
+    for (uint32_t i = tid; i < n; i += NT) sorted_idx[begin + i] = __ldg(src32 + 2 * (srcb[i] & smask));
     mm_sync<NT>();
   }
   if (!done) return;
