@@ -63,7 +63,7 @@ const char* kStageNames[kNumStages] = {"memset",    "project_count", "scan_tiles
 struct Scratch {
   Buf scat;  // unfused bilinear binning: depth key + tile block | corner mask per point
   Buf zeroed, cursor, big_tiles, huge_tiles, big_elem, big_chunk, entries, tmp, overflow, slots, agg, g_eval;
-  Buf chunk_alive;
+  Buf chunk_alive, mid_l2, mid_l3;  // k_sort_mid_merge size-class lists
 };
 
 struct ViewState {
@@ -85,7 +85,12 @@ struct inpc_ctx {
   int mid_grid = 0;       // k_sort_mid: resident CTAs (grid-stride over the big-tile list)
   bool no_mid_sort = false; // env INPC_NO_MID_SORT=1: every big tile through k_sort_big (A/B)
   bool mid_cta = false;     // env INPC_MID_SORT=cta: mid tiles through the CTA radix k_sort_mid (A/B)
-  int midw_grid[2] = {0, 0}; // k_sort_mid_merge (<= 1024, <= 2048 entries): resident CTAs
+  // env INPC_MERGE8K=1: tiles of 2049..8192 entries by the 512-thread merge sort
+  // (cfg 4: 1.755 -> 1.69 ms) instead of k_sort_big; off by default because the
+  // extra 70 KB-SMEM launch per view costs cfg 5 1.9 ms per 64-view step even
+  // with an empty list (it cannot co-reside with the other view stream's blends)
+  bool merge8k = false;
+  int midw_grid[3] = {0, 0, 0}; // k_sort_mid_merge (<= 1024, <= 2048, <= 8192 entries): resident CTAs
   // chunk bounds of a static cloud (inpc_ctx_set_chunks): used by forwards over that cloud
   const float* chunk_box = nullptr;
   const float* chunk_xyz = nullptr;
@@ -196,7 +201,7 @@ struct AllocScope {
 
 void release_all(inpc_ctx* c) {
   for (Scratch& x : c->scr)
-    for (Buf* b : {&x.chunk_alive, &x.scat, &x.zeroed, &x.cursor, &x.big_tiles, &x.huge_tiles, &x.big_elem,
+    for (Buf* b : {&x.mid_l2, &x.mid_l3, &x.chunk_alive, &x.scat, &x.zeroed, &x.cursor, &x.big_tiles, &x.huge_tiles, &x.big_elem,
                    &x.big_chunk, &x.entries, &x.slots, &x.agg, &x.g_eval, &x.tmp, &x.overflow})
       free_buf(*b);
   for (Buf* b : {&c->det_f, &c->det_o, &c->f4_rec, &c->f4_keys, &c->f4_vals, &c->f4_keys2, &c->f4_vals2, &c->f4_hist, &c->f4_scan,
@@ -562,9 +567,13 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
     c->no_mid_sort = e && e[0] == '1';
     const char* m = getenv("INPC_MID_SORT");
     c->mid_cta = m && !strcmp(m, "cta");
-    int o1 = 0, o2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_sort_mid_merge<64, 1024>, 64, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_sort_mid_merge<128, 2048>, 128, 0);
+    int o1 = 0, o2 = 0, o3 = 0;
+    cudaFuncSetAttribute(k_sort_mid_merge<512, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)MidMerge<512, 8192>::kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_sort_mid_merge<64, 1024>, 64, MidMerge<64, 1024>::kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_sort_mid_merge<128, 2048>, 128, MidMerge<128, 2048>::kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_sort_mid_merge<512, 8192>, 512, MidMerge<512, 8192>::kSmem);
+    c->midw_grid[2] = c->num_sms * (o3 > 0 ? o3 : 1);
     c->midw_grid[0] = c->num_sms * (o1 > 0 ? o1 : 1);
     c->midw_grid[1] = c->num_sms * (o2 > 0 ? o2 : 1);
   }
@@ -583,6 +592,8 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
   {
     const char* e = getenv("INPC_NO_FUSED_BIN");
     c->no_fused_bin = e && e[0] == '1';
+    const char* m8 = getenv("INPC_MERGE8K");
+    c->merge8k = m8 && m8[0] == '1';
     const char* r = getenv("INPC_REC16");
     c->rec16_pref = !(r && r[0] == '0');
   }
@@ -804,9 +815,11 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     if (!gauss && (st = ensure(X.slots, (size_t)(N > 0 ? N : 1) * 16, s))) return st;
     if ((st = ensure(X.big_tiles, (size_t)(T + 1) * 4, s))) return st;
     if ((st = ensure(X.huge_tiles, (size_t)(T + 1) * 4, s))) return st;
+    if ((st = ensure(X.mid_l2, (size_t)(T + 1) * 4, s))) return st;
+    if ((st = ensure(X.mid_l3, (size_t)(T + 1) * 4, s))) return st;
     if ((st = ensure(X.big_elem, (size_t)(T + 2) * 4, s))) return st;
     if ((st = ensure(X.big_chunk, (size_t)(T + 2) * 4, s))) return st;
-    // [0] Gaussian overflow flag, [6] k_sort_mid done counter
+    // [0] Gaussian overflow flag, [6] k_sort_mid / merge done counters [6..8]
     if ((st = ensure(X.overflow, 64, s, &fresh))) return st;
     if (fresh) CK(cudaMemsetAsync(X.overflow.p, 0, X.overflow.bytes, s));
     if (!sync_views) {
@@ -929,7 +942,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       uint32_t* ht = c->no_mid_sort ? nullptr : (uint32_t*)X.huge_tiles.p;
       k_scan_tiles<<<scan_blocks, kScanThreads, 0, sv>>>(T, tc, (uint32_t*)vs.ranges.p, (uint32_t*)X.cursor.p,
                                                          (uint32_t*)X.big_tiles.p, scan_state, scan_ctl, sc, ht,
-                                                         (uint32_t)kMidMax);
+                                                         (uint32_t)(c->mid_cta || !c->merge8k ? kMidMax : kMergeMax));
       CK(cudaGetLastError());
     }
     uint64_t need = need_v[v];
@@ -955,21 +968,30 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
                                                         (unsigned long long*)X.entries.p, scp, calive);
       CK(cudaGetLastError());
     }
-    if (N > kWarpSortCap && !fused_kp && !c->no_mid_sort) {  // tiles of 257..kMidMax entries
+    if (N > kWarpSortCap && !fused_kp && !c->no_mid_sort) {  // tiles of 257..kMergeMax entries
       StageTimer tm(c, sv, kStSortMid, 1);
       if (c->mid_cta) {
         k_sort_mid<<<c->mid_grid, kMidThreads, 0, sv>>>((const uint32_t*)vs.ranges.p, (const uint32_t*)X.big_tiles.p,
                                                         sc, (const unsigned long long*)X.entries.p,
                                                         (uint32_t*)vs.sorted_idx.p, (uint32_t*)X.overflow.p + 6);
-      } else {  // merge sort: tiles of 257..1024, then 1025..2048 (which clears the list)
+      } else {  // merge sort: tiles of 257..1024, 1025..2048, 2049..8192 (the last clears the list)
         const uint32_t* rp = (const uint32_t*)vs.ranges.p;
         const uint32_t* bp = (const uint32_t*)X.big_tiles.p;
         const unsigned long long* ep = (const unsigned long long*)X.entries.p;
         uint32_t* sp = (uint32_t*)vs.sorted_idx.p;
-        k_sort_mid_merge<64, 1024><<<c->midw_grid[0], 64, 0, sv>>>(rp, bp, sc, ep, sp, (uint32_t)kWarpSortCap, nullptr);
+        // each size class forwards its larger tiles to the next class's list
+        uint32_t* dn = (uint32_t*)X.overflow.p + 6;
+        uint32_t* l2 = (uint32_t*)X.mid_l2.p;
+        uint32_t* l3 = (uint32_t*)X.mid_l3.p;
+        k_sort_mid_merge<64, 1024><<<c->midw_grid[0], 64, MidMerge<64, 1024>::kSmem, sv>>>(
+            rp, bp, &sc->num_big, &sc->max_big, ep, sp, l2, &sc->num_l2, dn);
         CK(cudaGetLastError());
-        k_sort_mid_merge<128, 2048><<<c->midw_grid[1], 128, 0, sv>>>(rp, bp, sc, ep, sp, 1024u,
-                                                                      (uint32_t*)X.overflow.p + 6);
+        k_sort_mid_merge<128, 2048><<<c->midw_grid[1], 128, MidMerge<128, 2048>::kSmem, sv>>>(
+            rp, l2, &sc->num_l2, nullptr, ep, sp, c->merge8k ? l3 : nullptr, &sc->num_l3, dn + 1);
+        CK(cudaGetLastError());
+        if (c->merge8k)
+          k_sort_mid_merge<512, 8192><<<c->midw_grid[2], 512, MidMerge<512, 8192>::kSmem, sv>>>(
+              rp, l3, &sc->num_l3, nullptr, ep, sp, nullptr, nullptr, dn + 2);
       }
       CK(cudaGetLastError());
 #ifdef INPC_PHASE_TIMES
@@ -986,7 +1008,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     }
     if (N > kWarpSortCap && !fused_kp) {  // a tile can only exceed the cap with > cap points
       StageTimer tm(c, sv, kStSortBig, 1);
-      uint32_t min_n = c->no_mid_sort ? (uint32_t)kWarpSortCap : (uint32_t)kMidMax;
+      uint32_t min_n = c->no_mid_sort ? (uint32_t)kWarpSortCap : (uint32_t)(c->mid_cta || !c->merge8k ? kMidMax : kMergeMax);
       const uint32_t* r = (const uint32_t*)vs.ranges.p;
       const uint32_t* bt = (const uint32_t*)X.big_tiles.p;
       uint32_t* be = (uint32_t*)X.big_elem.p;

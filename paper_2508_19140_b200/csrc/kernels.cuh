@@ -386,7 +386,7 @@ struct ViewScalars {
   uint32_t pad;      // big-tile chunk dispenser (k_sort_big), zero between calls
   uint32_t num_huge;  // unfused path: tiles over kMidMax entries (k_sort_big's list; reset by it)
   uint32_t max_huge;  // largest of them
-  uint32_t pad2, pad3;
+  uint32_t num_l2, num_l3;  // k_sort_mid_merge: tiles of 1025..2048 / 2049..8192 entries (reset by their consumers)
 };
 
 // Scan bookkeeping, zero on entry and left zero on exit (the last CTA to
@@ -1521,6 +1521,7 @@ struct MidSort {
 };
 constexpr int kMidThreads = 128;
 constexpr int kMidMax = 2048;
+constexpr int kMergeMax = 8192;  // k_sort_mid_merge's largest tiles; k_sort_big takes the rest
 using MidCfg = MidSort<kMidThreads, kMidMax>;
 
 // Sort the n keys of S.s (slot order); returns true with S.k32 holding the
@@ -1755,9 +1756,10 @@ __global__ void __launch_bounds__(kMidThreads) k_sort_mid(const uint32_t* __rest
 // the latency of its ~400 dependent merge steps).
 template <int NT, int MAXN>
 struct MidMerge {
-  static constexpr int kSlotBits = MAXN == 1024 ? 10 : 11;
+  static constexpr int kSlotBits = MAXN == 1024 ? 10 : MAXN == 2048 ? 11 : MAXN == 4096 ? 12 : 13;
   static constexpr int kQMax = MAXN / NT + 1;     // keys per thread (odd: conflict-free thread strides)
   static constexpr int kBuf = NT * kQMax;         // padded tile length
+  static constexpr size_t kSmem = 2 * (size_t)kBuf * 4;  // two ping-pong buffers (dynamic SMEM)
   static constexpr int kMaxRun = 64;
   static_assert(MAXN == (1 << kSlotBits), "slot bits");
   static_assert(kQMax <= 17 && 2 * kBuf * 4 >= MAXN * 8, "run length / 64-bit fallback room");
@@ -1832,12 +1834,12 @@ __device__ __forceinline__ void mm_bitonic64(unsigned long long* s, int np, int 
 
 template <int NT, int MAXN>
 __global__ void __launch_bounds__(NT) k_sort_mid_merge(
-    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ big_tiles, ViewScalars* __restrict__ sc,
-    const unsigned long long* __restrict__ entries, uint32_t* __restrict__ sorted_idx, uint32_t lo_n,
-    uint32_t* __restrict__ done) {
+    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ list_in, uint32_t* count_in,
+    uint32_t* reset_also, const unsigned long long* __restrict__ entries, uint32_t* __restrict__ sorted_idx,
+    uint32_t* __restrict__ list_out, uint32_t* count_out, uint32_t* __restrict__ done) {
   using M = MidMerge<NT, MAXN>;
   constexpr int NW = NT / 32;
-  __shared__ __align__(16) uint32_t buf[2 * M::kBuf];
+  extern __shared__ __align__(16) uint32_t buf[];  // 2 * kBuf
   __shared__ uint32_t red[2][NW];
   __shared__ uint32_t s_last;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -1845,11 +1847,14 @@ __global__ void __launch_bounds__(NT) k_sort_mid_merge(
   uint32_t* buf1 = buf + M::kBuf;
   constexpr int SB = M::kSlotBits;
   constexpr uint32_t smask = (uint32_t)MAXN - 1u;
-  const uint32_t nb = sc->num_big;
+  const uint32_t nb = *count_in;
   for (uint32_t j = blockIdx.x; j < nb; j += gridDim.x) {
-    const uint32_t t = big_tiles[j];
+    const uint32_t t = list_in[j];
     const uint32_t begin = ranges[t], n = ranges[t + 1] - begin;
-    if (n <= lo_n || n > (uint32_t)MAXN) continue;  // block-uniform
+    if (n > (uint32_t)MAXN) {  // block-uniform: the next size class's list
+      if (list_out && tid == 0) list_out[atomicAdd(count_out, 1u)] = t;
+      continue;
+    }
     const unsigned long long* src = entries + begin;
     // depth bits to buf1, tile minimum / maximum
     uint32_t dlo = 0xFFFFFFFFu, dhi = 0u;
@@ -1967,8 +1972,7 @@ __global__ void __launch_bounds__(NT) k_sort_mid_merge(
     for (uint32_t i = tid; i < n; i += NT) sorted_idx[begin + i] = __ldg(src32 + 2 * (srcb[i] & smask));
     mm_sync<NT>();
   }
-  if (!done) return;
-  // the last CTA of the last mid kernel clears the list count for the next call
+  // the last CTA clears its input list's count for the next call
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -1977,8 +1981,8 @@ __global__ void __launch_bounds__(NT) k_sort_mid_merge(
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
     *done = 0u;
-    sc->num_big = 0u;
-    sc->max_big = 0u;
+    *count_in = 0u;
+    if (reset_also) *reset_also = 0u;
   }
 }
 

@@ -312,7 +312,9 @@ def test_unfused_binning_cfg2(inpc, ctx_unfused):
                                     (300, "none"), (2048, "short"),
                                     # warp merge sort of the mid tiles (257..1024, 1025..2048)
                                     (257, "none"), (513, "short"), (600, "short"), (700, "long"),
-                                    (1000, "none"), (1024, "short"), (1025, "long"), (1800, "none")])
+                                    (1000, "none"), (1024, "short"), (1025, "long"), (1800, "none"),
+                                    # ... 2049..8192 (512 threads per tile), k_sort_big above
+                                    (4100, "long"), (8192, "short"), (8193, "none")])
 def test_unfused_big_tile(inpc, ctx_unfused, n, ties):
     """k_sort_big: radix chunks (> 2048 entries) with short tie runs fixed up
     in index order, 32-bit-key bitonic chunks (<= 2048) with odd-even
@@ -476,3 +478,24 @@ def test_cfg5_multiview_sampled(inpc, ctx):
         gfo += o["g_feat"]; goo += o["g_opacity"]
     check_grads(gf.cpu().numpy(), gfo)
     check_grads(go.cpu().numpy(), goo)
+
+@pytest.fixture(scope="module")
+def ctx_merge8k(inpc):
+    """Unfused binning with the 512-thread merge sort for 2049..8192-entry tiles."""
+    import os
+    old = {k: os.environ.get(k) for k in ("INPC_NO_FUSED_BIN", "INPC_MERGE8K")}
+    os.environ["INPC_NO_FUSED_BIN"] = "1"
+    os.environ["INPC_MERGE8K"] = "1"
+    c = inpc.Context(0)
+    for k, v in old.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("n,ties", [(2049, "none"), (4100, "long"), (6000, "short"), (8192, "short"), (8193, "none")])
+def test_merge8k_big_tile(inpc, ctx_merge8k, n, ties):
+    test_one_hot_tile_over_smem_cap(inpc, ctx_merge8k, n, ties)
