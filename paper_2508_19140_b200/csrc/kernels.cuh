@@ -452,31 +452,63 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
   __syncthreads();
   const uint32_t excl = (wid ? warp_tot[wid - 1] : 0u) + x - sum;
   const uint32_t agg = warp_tot[kScanThreads / 32 - 1];
-  if (threadIdx.x == 0) {
+  if (wid == 0) {
     volatile unsigned long long* vs = state;
     if (bid == 0) {
-      vs[0] = (2ull << 32) | agg;
-      s_prefix = 0;
+      if (lane == 0) {
+        vs[0] = (2ull << 32) | agg;
+        s_prefix = 0;
+      }
     } else {
-      vs[bid] = (1ull << 32) | agg;
+      if (lane == 0) vs[bid] = (1ull << 32) | agg;
+      // warp-parallel look-back: 32 predecessors per round (one L2 round trip
+      // instead of one per predecessor)
       uint32_t prefix = 0;
       int b = (int)bid - 1;
       while (true) {
-        unsigned long long v = vs[b];
-        uint32_t flag = (uint32_t)(v >> 32);
-        if (flag == 0) continue;  // predecessor not published yet
-        prefix += (uint32_t)v;
-        if (flag == 2) break;
-        --b;
+        const int idx = b - lane;
+        const unsigned long long v = idx >= 0 ? vs[idx] : (2ull << 32);
+        const uint32_t flag = (uint32_t)(v >> 32);
+        const unsigned inc = __ballot_sync(0xffffffffu, flag == 2u);
+        const unsigned zero = __ballot_sync(0xffffffffu, flag == 0u);
+        const int first = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive prefix
+        const unsigned upto = first == 32 ? 0xffffffffu : ((2u << first) - 1u);
+        if (zero & upto) continue;  // a predecessor before it has not published yet
+        prefix += __reduce_add_sync(0xffffffffu, ((1u << lane) & upto) ? (uint32_t)v : 0u);
+        if (first < 32) break;
+        b -= 32;
       }
-      __threadfence();
-      vs[bid] = (2ull << 32) | (prefix + agg);
-      s_prefix = prefix;
+      if (lane == 0) {
+        __threadfence();
+        vs[bid] = (2ull << 32) | (prefix + agg);
+        s_prefix = prefix;
+      }
     }
   }
   __syncthreads();
   uint32_t off = s_prefix + excl, mxh = 0u;
   const unsigned lt = (1u << lane) - 1u;
+  // big-tile lists: one atomic per warp for all its items (the list order is
+  // free), so no item waits on an atomic round trip
+  unsigned bm[kScanItems], hm[kScanItems];
+  uint32_t nbig = 0u, nhuge = 0u;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const bool in = i0 + k < T;
+    const bool big = in && c[k] > (uint32_t)kWarpSortCap;
+    const bool huge = big && huge_tiles && c[k] > huge_min;  // also on k_sort_big's own list
+    bm[k] = __ballot_sync(0xffffffffu, big);
+    hm[k] = __ballot_sync(0xffffffffu, huge);
+    nbig += __popc(bm[k]);
+    nhuge += __popc(hm[k]);
+  }
+  uint32_t bb = 0u, hb = 0u;
+  if (lane == 0) {
+    if (nbig) bb = atomicAdd(&sc->num_big, nbig);
+    if (nhuge) hb = atomicAdd(&sc->num_huge, nhuge);
+  }
+  bb = __shfl_sync(0xffffffffu, bb, 0);
+  hb = __shfl_sync(0xffffffffu, hb, 0);
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     const bool in = i0 + k < T;
@@ -484,29 +516,16 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
       ranges[i0 + k] = off;
       cursor[i0 + k] = off;
     }
-    // big-tile lists: one atomic per warp and item (the list order is free)
-    const bool big = in && c[k] > (uint32_t)kWarpSortCap;
-    const unsigned bm = __ballot_sync(0xffffffffu, big);
-    if (bm) {
-      uint32_t base = 0u;
-      if (lane == __ffs(bm) - 1) base = atomicAdd(&sc->num_big, (uint32_t)__popc(bm));
-      base = __shfl_sync(0xffffffffu, base, __ffs(bm) - 1);
-      if (big) {
-        big_tiles[base + __popc(bm & lt)] = i0 + k;
-        mx = max(mx, c[k]);
-      }
-      const bool huge = big && huge_tiles && c[k] > huge_min;  // also on k_sort_big's own list
-      const unsigned hm = __ballot_sync(0xffffffffu, huge);
-      if (hm) {
-        uint32_t hb = 0u;
-        if (lane == __ffs(hm) - 1) hb = atomicAdd(&sc->num_huge, (uint32_t)__popc(hm));
-        hb = __shfl_sync(0xffffffffu, hb, __ffs(hm) - 1);
-        if (huge) {
-          huge_tiles[hb + __popc(hm & lt)] = i0 + k;
-          mxh = max(mxh, c[k]);
-        }
-      }
+    if ((bm[k] >> lane) & 1u) {
+      big_tiles[bb + __popc(bm[k] & lt)] = i0 + k;
+      mx = max(mx, c[k]);
     }
+    if ((hm[k] >> lane) & 1u) {
+      huge_tiles[hb + __popc(hm[k] & lt)] = i0 + k;
+      mxh = max(mxh, c[k]);
+    }
+    bb += __popc(bm[k]);
+    hb += __popc(hm[k]);
     off += c[k];
   }
   if (mx) atomicMax(&sc->max_big, mx);
