@@ -85,11 +85,13 @@ struct inpc_ctx {
   int mid_grid = 0;       // k_sort_mid: resident CTAs (grid-stride over the big-tile list)
   bool no_mid_sort = false; // env INPC_NO_MID_SORT=1: every big tile through k_sort_big (A/B)
   bool mid_cta = false;     // env INPC_MID_SORT=cta: mid tiles through the CTA radix k_sort_mid (A/B)
-  // env INPC_MERGE8K=1: tiles of 2049..8192 entries by the 512-thread merge sort
-  // (cfg 4: 1.755 -> 1.69 ms) instead of k_sort_big; off by default because the
-  // extra 70 KB-SMEM launch per view costs cfg 5 1.9 ms per 64-view step even
-  // with an empty list (it cannot co-reside with the other view stream's blends)
-  bool merge8k = false;
+  // tiles of 2049..8192 entries by the 512-thread merge sort instead of
+  // k_sort_big (cfg 4: 1.755 -> 1.69 ms) for dense clouds (N >= 512 T), where
+  // such tiles are likely; not for sparser ones, where the extra 70 KB-SMEM
+  // launch per view costs (cfg 5: 1.9 ms per 64-view step with an empty list:
+  // it cannot co-reside with the other view stream's blends).  Either way every
+  // tile is sorted; env INPC_MERGE8K=0 / 1 forces the choice (A/B).
+  int merge8k_env = -1;
   int midw_grid[3] = {0, 0, 0}; // k_sort_mid_merge (<= 1024, <= 2048, <= 8192 entries): resident CTAs
   // chunk bounds of a static cloud (inpc_ctx_set_chunks): used by forwards over that cloud
   const float* chunk_box = nullptr;
@@ -593,7 +595,7 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
     const char* e = getenv("INPC_NO_FUSED_BIN");
     c->no_fused_bin = e && e[0] == '1';
     const char* m8 = getenv("INPC_MERGE8K");
-    c->merge8k = m8 && m8[0] == '1';
+    c->merge8k_env = m8 ? (m8[0] == '1' ? 1 : 0) : -1;
     const char* r = getenv("INPC_REC16");
     c->rec16_pref = !(r && r[0] == '0');
   }
@@ -774,6 +776,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
         break;
       }
   }
+  const bool merge8k = c->merge8k_env >= 0 ? c->merge8k_env == 1 : N >= 512 * (int64_t)T;
   // unfused bilinear binning: 16-byte records {u, v, z, o}, the blends read
   // the features from feat (measured on cfg 5: see DESIGN.md)
   const bool rec16 = c->rec16_pref && !gauss && !sh && !debug && !fused_kp && N > 0 && T < (1 << 28);
@@ -942,7 +945,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       uint32_t* ht = c->no_mid_sort ? nullptr : (uint32_t*)X.huge_tiles.p;
       k_scan_tiles<<<scan_blocks, kScanThreads, 0, sv>>>(T, tc, (uint32_t*)vs.ranges.p, (uint32_t*)X.cursor.p,
                                                          (uint32_t*)X.big_tiles.p, scan_state, scan_ctl, sc, ht,
-                                                         (uint32_t)(c->mid_cta || !c->merge8k ? kMidMax : kMergeMax));
+                                                         (uint32_t)(c->mid_cta || !merge8k ? kMidMax : kMergeMax));
       CK(cudaGetLastError());
     }
     uint64_t need = need_v[v];
@@ -987,9 +990,9 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
             rp, bp, &sc->num_big, &sc->max_big, ep, sp, l2, &sc->num_l2, dn);
         CK(cudaGetLastError());
         k_sort_mid_merge<128, 2048><<<c->midw_grid[1], 128, MidMerge<128, 2048>::kSmem, sv>>>(
-            rp, l2, &sc->num_l2, nullptr, ep, sp, c->merge8k ? l3 : nullptr, &sc->num_l3, dn + 1);
+            rp, l2, &sc->num_l2, nullptr, ep, sp, merge8k ? l3 : nullptr, &sc->num_l3, dn + 1);
         CK(cudaGetLastError());
-        if (c->merge8k)
+        if (merge8k)
           k_sort_mid_merge<512, 8192><<<c->midw_grid[2], 512, MidMerge<512, 8192>::kSmem, sv>>>(
               rp, l3, &sc->num_l3, nullptr, ep, sp, nullptr, nullptr, dn + 2);
       }
@@ -1008,7 +1011,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     }
     if (N > kWarpSortCap && !fused_kp) {  // a tile can only exceed the cap with > cap points
       StageTimer tm(c, sv, kStSortBig, 1);
-      uint32_t min_n = c->no_mid_sort ? (uint32_t)kWarpSortCap : (uint32_t)(c->mid_cta || !c->merge8k ? kMidMax : kMergeMax);
+      uint32_t min_n = c->no_mid_sort ? (uint32_t)kWarpSortCap : (uint32_t)(c->mid_cta || !merge8k ? kMidMax : kMergeMax);
       const uint32_t* r = (const uint32_t*)vs.ranges.p;
       const uint32_t* bt = (const uint32_t*)X.big_tiles.p;
       uint32_t* be = (uint32_t*)X.big_elem.p;
@@ -1049,6 +1052,18 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     for (int k = 0; k < nsets; ++k) {
       CK(cudaEventRecord(c->ev_join[k], c->vstream[k]));
       CK(cudaStreamWaitEvent(s, c->ev_join[k], 0));
+    }
+  }
+  if (gauss && debug) {  // assertion of the capacity bound (gauss_tiles_bound): the scatter flags any dropped entry
+    for (int k = 0; k < nsets; ++k) {
+      uint32_t flag = 0;
+      CK(cudaMemcpyAsync(&flag, c->scr[k].overflow.p, 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (flag) {
+        CK(cudaMemsetAsync(c->scr[k].overflow.p, 0, 4, s));
+        g_last_error = "Gaussian fragment capacity exceeded (entries dropped)";
+        return INPC_KEY_OVERFLOW;
+      }
     }
   }
   c->have_state = true;

@@ -3,8 +3,8 @@
 # one --set full launch of each cfg5 kernel, cfg2 kernels, the dominant kernel of cfg3 / cfg4 / variants
 mkdir -p gpurun_out/prof_out
 B="python bench.py --steps 1 --warmup 3 --profile-run --no-graph --no-cpu-baseline"
-# launch list: skip the stats forward + 3 warm-up steps of 64 views (~7 kernels per view), keep one step
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" -s 1800 -c 460 --csv \
+# launch list: skip the stats forward (64 x 7 kernels) + 3 warm-up steps of 64 views (8 kernels per view), keep one step
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" -s 1984 -c 512 --csv \
     --log-file gpurun_out/launches_r02.csv $B > /dev/null 2>&1
 for k in k_blend_bwd k_blend_fwd k_sort_mid k_project_count k_scatter_slots k_scan_tiles; do
   ncu --set full --clock-control none --import-source on -k regex:"$k" -s 70 -c 1 -o gpurun_out/prof_r02_cfg5_$k $B > /dev/null 2>&1
