@@ -387,6 +387,8 @@ struct ViewScalars {
   uint32_t num_huge;  // unfused path: tiles over kMidMax entries (k_sort_big's list; reset by it)
   uint32_t max_huge;  // largest of them
   uint32_t num_l2, num_l3;  // k_sort_mid_merge: tiles of 1025..2048 / 2049..8192 entries (reset by their consumers)
+  uint32_t num_small;       // k_scan_tiles: tiles placed at the end of the blend order (reset by its last CTA)
+  uint32_t pad4, pad5, pad6;
 };
 
 // Scan bookkeeping, zero on entry and left zero on exit (the last CTA to
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
     int T, uint32_t* __restrict__ count, uint32_t* __restrict__ ranges,
     uint32_t* __restrict__ cursor, uint32_t* __restrict__ big_tiles,
     unsigned long long* state, ScanCtl* ctl, ViewScalars* sc, uint32_t* __restrict__ huge_tiles,
-    uint32_t huge_min) {
+    uint32_t huge_min, uint32_t* __restrict__ order) {
   __shared__ uint32_t warp_tot[kScanThreads / 32];
   __shared__ uint32_t s_prefix, s_bid;
   if (threadIdx.x == 0) s_bid = atomicAdd(&ctl->ticket, 1u);
@@ -490,8 +492,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
   const unsigned lt = (1u << lane) - 1u;
   // big-tile lists: one atomic per warp for all its items (the list order is
   // free), so no item waits on an atomic round trip
-  unsigned bm[kScanItems], hm[kScanItems];
-  uint32_t nbig = 0u, nhuge = 0u;
+  // blend order (optional): big tiles first (positions of the big list), the
+  // others from the end, so the long tiles do not start last
+  unsigned bm[kScanItems], hm[kScanItems], sm[kScanItems];
+  uint32_t nbig = 0u, nhuge = 0u, nsmall = 0u;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     const bool in = i0 + k < T;
@@ -499,16 +503,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
     const bool huge = big && huge_tiles && c[k] > huge_min;  // also on k_sort_big's own list
     bm[k] = __ballot_sync(0xffffffffu, big);
     hm[k] = __ballot_sync(0xffffffffu, huge);
+    sm[k] = __ballot_sync(0xffffffffu, in && !big && order != nullptr);
     nbig += __popc(bm[k]);
     nhuge += __popc(hm[k]);
+    nsmall += __popc(sm[k]);
   }
-  uint32_t bb = 0u, hb = 0u;
+  uint32_t bb = 0u, hb = 0u, sb = 0u;
   if (lane == 0) {
     if (nbig) bb = atomicAdd(&sc->num_big, nbig);
     if (nhuge) hb = atomicAdd(&sc->num_huge, nhuge);
+    if (nsmall) sb = atomicAdd(&sc->num_small, nsmall);
   }
   bb = __shfl_sync(0xffffffffu, bb, 0);
   hb = __shfl_sync(0xffffffffu, hb, 0);
+  sb = __shfl_sync(0xffffffffu, sb, 0);
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     const bool in = i0 + k < T;
@@ -518,8 +526,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
     }
     if ((bm[k] >> lane) & 1u) {
       big_tiles[bb + __popc(bm[k] & lt)] = i0 + k;
+      if (order) order[bb + __popc(bm[k] & lt)] = i0 + k;
       mx = max(mx, c[k]);
     }
+    if ((sm[k] >> lane) & 1u) order[T - 1 - (sb + __popc(sm[k] & lt))] = i0 + k;
+    sb += __popc(sm[k]);
     if ((hm[k] >> lane) & 1u) {
       huge_tiles[hb + __popc(hm[k] & lt)] = i0 + k;
       mxh = max(mxh, c[k]);
@@ -546,6 +557,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
     if (threadIdx.x == 0) {
       ctl->ticket = 0u;
       ctl->done = 0u;
+      sc->num_small = 0u;
     }
   }
 }
@@ -2480,6 +2492,7 @@ struct BlendOut {
   int32_t* ncontrib;  // or null
   float* T_final;     // saved [H,W]
   uint32_t* last;     // saved [H,W]: list position + 1 of the last composited fragment
+  const uint32_t* order;  // tile visiting order (big tiles first) or null: band order
 };
 
 template <int CMAX>
@@ -2588,7 +2601,7 @@ __global__ void __launch_bounds__(WPB * 32, INPC_FWD_MINB) k_blend_fwd(
   FwdSmem<CMAX, PF>& S = reinterpret_cast<FwdSmem<CMAX, PF>*>(smem_raw)[warp];
   const int tl = blockIdx.x * WPB + warp;
   if (tl >= band_tiles) return;  // warp-uniform; no block barriers below
-  const int tile = g.ty0 * g.tiles_x + tl;
+  const int tile = out.order ? (int)out.order[tl] : g.ty0 * g.tiles_x + tl;
   const int tx0 = (tile % g.tiles_x) * kTile, ty0 = (tile / g.tiles_x) * kTile;
   const int px = tx0 + (lane & 7), pyA = ty0 + (lane >> 3), pyB = pyA + 4;
   const int pcA = 2 * (lane >> 3) + (lane & 7);  // 2 ly + lx of pixel A (B: + 8)
@@ -2658,6 +2671,7 @@ struct BwdIn {
   // k_det_reduce adds them per point in a fixed order
   float* det_f;
   float* det_o;
+  const uint32_t* order;  // tile visiting order or null (as the forward's)
 };
 
 template <int CMAX>
@@ -2795,7 +2809,7 @@ __global__ void __launch_bounds__(WPB * 32, CMAX <= 4 ? INPC_BWD_WARPS_PER_SM / 
   SM& S = reinterpret_cast<SM*>(smem_raw)[warp];
   const int tl = blockIdx.x * WPB + warp;
   if (tl >= band_tiles) return;
-  const int tile = g.ty0 * g.tiles_x + tl;
+  const int tile = in.order ? (int)in.order[tl] : g.ty0 * g.tiles_x + tl;
   const int tx0 = (tile % g.tiles_x) * kTile, ty0 = (tile / g.tiles_x) * kTile;
   const int px = tx0 + (lane & 7), pyA = ty0 + (lane >> 3), pyB = pyA + 4;
   const int pcA = 2 * (lane >> 3) + (lane & 7);  // 2 ly + lx of pixel A (B: + 8)

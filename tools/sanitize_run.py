@@ -42,15 +42,25 @@ def main():
     run(ctx_u, c2)
     run(ctx, c1, "gaussian", sigma=0.0)
     if which == "all":
-        # one dense tile (mid sort) and one huge tile (big sort + merges)
-        for n in (1500, 9000):
+        # dense tiles: the merge-sort classes (<= 1024, <= 2048, and <= 8192 with
+        # INPC_MERGE8K=1) with and without long depth-tie runs (64-bit bitonic
+        # fallback), and one huge tile (k_sort_big chunks + merges)
+        os.environ["INPC_NO_FUSED_BIN"] = "1"
+        os.environ["INPC_MERGE8K"] = "1"
+        ctx_m8 = inpc.Context(0)
+        del os.environ["INPC_NO_FUSED_BIN"]
+        del os.environ["INPC_MERGE8K"]
+        for n, ties, cx in ((300, False, ctx_u), (700, True, ctx_u), (1500, False, ctx_u), (1500, True, ctx_u),
+                            (9000, False, ctx_u), (5000, True, ctx_m8), (7000, False, ctx_m8)):
             rng = np.random.default_rng(n)
             cam = synthgen.camera(np.eye(3), np.zeros(3), 64.0, 64.0, 32, 32, 0.1)
             u = rng.uniform(17, 23, n); v = rng.uniform(9, 15, n); z = rng.uniform(1, 4, n)
+            if ties:
+                z[: n // 10] = 2.0
             xyz = np.stack([(u - 32) / 64 * z, (v - 32) / 64 * z, z], 1).astype(np.float32)
             c = dict(xyz=xyz, feat=rng.uniform(-1, 1, (n, 4)).astype(np.float32),
                      opacity=rng.uniform(0, 0.05, n).astype(np.float32), cams=[cam], H=64, W=64)
-            run(ctx_u, c, t_min=0.0)
+            run(cx, c, t_min=0.0)
         sh = np.random.default_rng(1).normal(0, 0.5, (1000, 4, 9)).astype(np.float32)
         cfg = inpc.make_cfg(64, 64, 4, flags=inpc.FLAG_SH_FEATURES)
         ctx.forward(cfg, c1["cams"], dev(c1["xyz"]), dev(sh), dev(c1["opacity"]))
