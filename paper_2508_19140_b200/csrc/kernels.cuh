@@ -25,7 +25,10 @@
 
 namespace inpc {
 
-constexpr int kWarpsPerBlock = 4;    // blend kernels: one warp per tile
+#ifndef INPC_WPB
+#define INPC_WPB 4
+#endif
+constexpr int kWarpsPerBlock = INPC_WPB;  // blend kernels: one warp per tile, WPB warps per CTA
 constexpr int kWarpSortCap = 256;    // tiles above this go through k_sort_big
 constexpr int kBigChunk = 2048;      // chunk of k_sort_big's SMEM sort (16 KB of keys)
 constexpr int kBigThreads = 512;
@@ -2586,7 +2589,7 @@ __device__ __forceinline__ void write_pixel(const DevCam& cam, const DevCfg& g, 
 // without).
 template <int MODE, int CMAX, bool COUNT, int WPB = kWarpsPerBlock, bool PF = false>
 #ifndef INPC_FWD_MINB
-#define INPC_FWD_MINB 8  // 64 registers (measured optimum: 76 at 1, 48 + spills at 10 are slower)
+#define INPC_FWD_MINB (32 / INPC_WPB)  // 64 registers (measured optimum: 76 at 1 CTA, 48 + spills at 40 warps are slower)
 #endif
 #ifndef INPC_BWD_WARPS_PER_SM
 #define INPC_BWD_WARPS_PER_SM 28
