@@ -109,7 +109,7 @@ struct inpc_ctx {
   int bin_grid[3] = {0, 0, 0};  // cooperative grid of k_bin_bilinear<2,4,8>
   bool no_fused_bin = false;     // env INPC_NO_FUSED_BIN=1: separate binning kernels
   bool rec16_pref = true;        // env INPC_REC16=0: 32-byte records with packed features (A/B)
-  bool tile_order_pref = true;   // env INPC_TILE_ORDER=0: blends visit tiles in raster order (A/B)
+  int tile_order_mode = 1;       // env INPC_TILE_ORDER: 0 raster order; 1 big first for one-view calls; 2 / 3: also even / all views of batches (A/B)
   bool rec16 = false;            // saved state: the forward wrote 16-byte records
   uint64_t entry_cap = 0;
   std::vector<ViewState> views;
@@ -599,7 +599,7 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
     const char* m8 = getenv("INPC_MERGE8K");
     c->merge8k_env = m8 ? (m8[0] == '1' ? 1 : 0) : -1;
     const char* to = getenv("INPC_TILE_ORDER");
-    c->tile_order_pref = !(to && to[0] == '0');
+    c->tile_order_mode = to ? atoi(to) : 1;
     const char* r = getenv("INPC_REC16");
     c->rec16_pref = !(r && r[0] == '0');
   }
@@ -790,7 +790,8 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
   // batches, whose two view streams already fill each other's kernel tails
   // (cfg 5 per-kernel times -6 %, but the overlapped step +2 %), nor Gaussian
   // (cfg 3 +2 %).
-  const bool use_order = c->tile_order_pref && V == 1 && !gauss && !fused_kp && g.ty0 == 0 && g.ty1 == g.tiles_y;
+  const bool use_order = c->tile_order_mode > 0 && (V == 1 || c->tile_order_mode >= 2) && !gauss && !fused_kp &&
+                         g.ty0 == 0 && g.ty1 == g.tiles_y;
   if (rec16) packed = false;
   // entry capacity per view: bilinear 4N; Gaussian a static bound when it
   // fits a quarter of the free memory (sync-free), else F_t read back per view
@@ -849,8 +850,8 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
     if ((st = ensure(vs.ranges, (size_t)(T + 1) * 4, s))) return st;
     if ((st = ensure(vs.T_final, (size_t)P * 4, s))) return st;
     if ((st = ensure(vs.last, (size_t)P * 4, s))) return st;
-    if (use_order && (st = ensure(vs.order, (size_t)T * 4, s))) return st;
-    vs.has_order = use_order;
+    vs.has_order = use_order && (c->tile_order_mode != 2 || V == 1 || v % 2 == 0);
+    if (vs.has_order && (st = ensure(vs.order, (size_t)T * 4, s))) return st;
     if ((st = ensure(vs.scalars, sizeof(ViewScalars), s, &fresh))) return st;
     if (fresh) CK(cudaMemsetAsync(vs.scalars.p, 0, vs.scalars.bytes, s));
     if ((st = ensure(vs.rec, (size_t)(N > 0 ? N : 1) * sizeof(PointRec), s))) return st;
@@ -959,7 +960,7 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       k_scan_tiles<<<scan_blocks, kScanThreads, 0, sv>>>(T, tc, (uint32_t*)vs.ranges.p, (uint32_t*)X.cursor.p,
                                                          (uint32_t*)X.big_tiles.p, scan_state, scan_ctl, sc, ht,
                                                          (uint32_t)(c->mid_cta || !merge8k ? kMidMax : kMergeMax),
-                                                         use_order ? (uint32_t*)vs.order.p : nullptr);
+                                                         vs.has_order ? (uint32_t*)vs.order.p : nullptr);
       CK(cudaGetLastError());
     }
     uint64_t need = need_v[v];

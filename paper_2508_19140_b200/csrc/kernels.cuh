@@ -390,7 +390,7 @@ struct ViewScalars {
   uint32_t num_huge;  // unfused path: tiles over kMidMax entries (k_sort_big's list; reset by it)
   uint32_t max_huge;  // largest of them
   uint32_t num_l2, num_l3;  // k_sort_mid_merge: tiles of 1025..2048 / 2049..8192 entries (reset by their consumers)
-  uint32_t num_small;       // k_scan_tiles: tiles placed at the end of the blend order (reset by its last CTA)
+  uint32_t pad7;
   uint32_t pad4, pad5, pad6;
 };
 
@@ -403,22 +403,26 @@ struct ScanCtl {
 
 // Decoupled look-back scan (one pass over the counts): each CTA scans
 // kScanTile counts, publishes its aggregate, and adds the prefix found by
-// walking back over its predecessors' published values.
-// state[b] = flag << 32 | value, flag 1 = aggregate, 2 = inclusive prefix.
+// walking back over its predecessors' published values.  Two prefixes in one
+// pass: entries (tile ranges) and big tiles (> kWarpSortCap entries), so the
+// big-tile list is in raster order with no atomics, and so is the optional
+// blend order (big tiles first, the others after them in reverse raster
+// order: neighbouring warps blend neighbouring tiles).
+// state[b] = flag << 62 | big << 32 | entries, flag 1 = aggregate, 2 = inclusive prefix.
 // The counts are zeroed as they are consumed (ready for the next call).
 __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
     int T, uint32_t* __restrict__ count, uint32_t* __restrict__ ranges,
     uint32_t* __restrict__ cursor, uint32_t* __restrict__ big_tiles,
     unsigned long long* state, ScanCtl* ctl, ViewScalars* sc, uint32_t* __restrict__ huge_tiles,
     uint32_t huge_min, uint32_t* __restrict__ order) {
-  __shared__ uint32_t warp_tot[kScanThreads / 32];
-  __shared__ uint32_t s_prefix, s_bid;
+  __shared__ uint32_t warp_tot[kScanThreads / 32], warp_big[kScanThreads / 32];
+  __shared__ uint32_t s_prefix, s_bprefix, s_bid;
   if (threadIdx.x == 0) s_bid = atomicAdd(&ctl->ticket, 1u);
   __syncthreads();
   const uint32_t bid = s_bid;
   const int i0 = bid * kScanTile + threadIdx.x * kScanItems;
   uint32_t c[kScanItems];
-  uint32_t sum = 0, mx = 0;
+  uint32_t sum = 0, nb = 0, mx = 0;
   if (i0 + kScanItems <= T) {
     uint4* p = reinterpret_cast<uint4*>(count + i0);
     const uint4 a = p[0], b = p[1];
@@ -434,111 +438,121 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
     }
   }
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) sum += c[k];
-  // block exclusive scan of the per-thread sums
+  for (int k = 0; k < kScanItems; ++k) {
+    sum += c[k];
+    nb += c[k] > (uint32_t)kWarpSortCap ? 1u : 0u;
+  }
+  // block exclusive scans of the per-thread sums (entries, big tiles)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t x = sum;
+  uint32_t x = sum, xb = nb;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    const uint32_t yb = __shfl_up_sync(0xffffffffu, xb, o);
+    if (lane >= o) {
+      x += y;
+      xb += yb;
+    }
   }
-  if (lane == 31) warp_tot[wid] = x;
+  if (lane == 31) {
+    warp_tot[wid] = x;
+    warp_big[wid] = xb;
+  }
   __syncthreads();
   if (wid == 0) {
     uint32_t w = lane < kScanThreads / 32 ? warp_tot[lane] : 0u;
+    uint32_t wb = lane < kScanThreads / 32 ? warp_big[lane] : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      const uint32_t yb = __shfl_up_sync(0xffffffffu, wb, o);
+      if (lane >= o) {
+        w += y;
+        wb += yb;
+      }
     }
-    if (lane < kScanThreads / 32) warp_tot[lane] = w;
+    if (lane < kScanThreads / 32) {
+      warp_tot[lane] = w;
+      warp_big[lane] = wb;
+    }
   }
   __syncthreads();
   const uint32_t excl = (wid ? warp_tot[wid - 1] : 0u) + x - sum;
+  const uint32_t bexcl = (wid ? warp_big[wid - 1] : 0u) + xb - nb;
   const uint32_t agg = warp_tot[kScanThreads / 32 - 1];
+  const uint32_t bagg = warp_big[kScanThreads / 32 - 1];
   if (wid == 0) {
     volatile unsigned long long* vs = state;
+    const unsigned long long mine = ((unsigned long long)bagg << 32) | agg;
     if (bid == 0) {
       if (lane == 0) {
-        vs[0] = (2ull << 32) | agg;
+        vs[0] = (2ull << 62) | mine;
         s_prefix = 0;
+        s_bprefix = 0;
       }
     } else {
-      if (lane == 0) vs[bid] = (1ull << 32) | agg;
+      if (lane == 0) vs[bid] = (1ull << 62) | mine;
       // warp-parallel look-back: 32 predecessors per round (one L2 round trip
       // instead of one per predecessor)
-      uint32_t prefix = 0;
+      uint32_t prefix = 0, bprefix = 0;
       int b = (int)bid - 1;
       while (true) {
         const int idx = b - lane;
-        const unsigned long long v = idx >= 0 ? vs[idx] : (2ull << 32);
-        const uint32_t flag = (uint32_t)(v >> 32);
+        const unsigned long long v = idx >= 0 ? vs[idx] : (2ull << 62);
+        const uint32_t flag = (uint32_t)(v >> 62);
         const unsigned inc = __ballot_sync(0xffffffffu, flag == 2u);
         const unsigned zero = __ballot_sync(0xffffffffu, flag == 0u);
         const int first = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive prefix
         const unsigned upto = first == 32 ? 0xffffffffu : ((2u << first) - 1u);
         if (zero & upto) continue;  // a predecessor before it has not published yet
-        prefix += __reduce_add_sync(0xffffffffu, ((1u << lane) & upto) ? (uint32_t)v : 0u);
+        const bool take = ((1u << lane) & upto) != 0u;
+        prefix += __reduce_add_sync(0xffffffffu, take ? (uint32_t)v : 0u);
+        bprefix += __reduce_add_sync(0xffffffffu, take ? (uint32_t)(v >> 32) & 0x3FFFFFFFu : 0u);
         if (first < 32) break;
         b -= 32;
       }
       if (lane == 0) {
         __threadfence();
-        vs[bid] = (2ull << 32) | (prefix + agg);
+        vs[bid] = (2ull << 62) | ((unsigned long long)(bprefix + bagg) << 32) | (prefix + agg);
         s_prefix = prefix;
+        s_bprefix = bprefix;
       }
     }
   }
   __syncthreads();
-  uint32_t off = s_prefix + excl, mxh = 0u;
+  uint32_t off = s_prefix + excl, bpos = s_bprefix + bexcl, mxh = 0u;
   const unsigned lt = (1u << lane) - 1u;
-  // big-tile lists: one atomic per warp for all its items (the list order is
-  // free), so no item waits on an atomic round trip
-  // blend order (optional): big tiles first (positions of the big list), the
-  // others from the end, so the long tiles do not start last
-  unsigned bm[kScanItems], hm[kScanItems], sm[kScanItems];
-  uint32_t nbig = 0u, nhuge = 0u, nsmall = 0u;
+  // huge list (rare): one atomic per warp for all its items
+  unsigned hm[kScanItems];
+  uint32_t nhuge = 0u;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    const bool in = i0 + k < T;
-    const bool big = in && c[k] > (uint32_t)kWarpSortCap;
-    const bool huge = big && huge_tiles && c[k] > huge_min;  // also on k_sort_big's own list
-    bm[k] = __ballot_sync(0xffffffffu, big);
+    const bool huge = huge_tiles && i0 + k < T && c[k] > (uint32_t)kWarpSortCap && c[k] > huge_min;
     hm[k] = __ballot_sync(0xffffffffu, huge);
-    sm[k] = __ballot_sync(0xffffffffu, in && !big && order != nullptr);
-    nbig += __popc(bm[k]);
     nhuge += __popc(hm[k]);
-    nsmall += __popc(sm[k]);
   }
-  uint32_t bb = 0u, hb = 0u, sb = 0u;
-  if (lane == 0) {
-    if (nbig) bb = atomicAdd(&sc->num_big, nbig);
-    if (nhuge) hb = atomicAdd(&sc->num_huge, nhuge);
-    if (nsmall) sb = atomicAdd(&sc->num_small, nsmall);
-  }
-  bb = __shfl_sync(0xffffffffu, bb, 0);
+  uint32_t hb = 0u;
+  if (lane == 0 && nhuge) hb = atomicAdd(&sc->num_huge, nhuge);
   hb = __shfl_sync(0xffffffffu, hb, 0);
-  sb = __shfl_sync(0xffffffffu, sb, 0);
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    const bool in = i0 + k < T;
-    if (in) {
-      ranges[i0 + k] = off;
-      cursor[i0 + k] = off;
+    const int t = i0 + k;
+    if (t < T) {
+      ranges[t] = off;
+      cursor[t] = off;
+      if (c[k] > (uint32_t)kWarpSortCap) {
+        big_tiles[bpos] = (uint32_t)t;
+        if (order) order[bpos] = (uint32_t)t;
+        mx = max(mx, c[k]);
+        ++bpos;
+      } else if (order) {
+        order[T - 1 - ((uint32_t)t - bpos)] = (uint32_t)t;  // t - bpos small tiles precede t
+      }
     }
-    if ((bm[k] >> lane) & 1u) {
-      big_tiles[bb + __popc(bm[k] & lt)] = i0 + k;
-      if (order) order[bb + __popc(bm[k] & lt)] = i0 + k;
-      mx = max(mx, c[k]);
-    }
-    if ((sm[k] >> lane) & 1u) order[T - 1 - (sb + __popc(sm[k] & lt))] = i0 + k;
-    sb += __popc(sm[k]);
     if ((hm[k] >> lane) & 1u) {
-      huge_tiles[hb + __popc(hm[k] & lt)] = i0 + k;
+      huge_tiles[hb + __popc(hm[k] & lt)] = t;
       mxh = max(mxh, c[k]);
     }
-    bb += __popc(bm[k]);
     hb += __popc(hm[k]);
     off += c[k];
   }
@@ -547,6 +561,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
   if (i0 < T && i0 + kScanItems >= T) {  // the thread owning the last tile
     ranges[T] = off;
     sc->Ft = off;
+    sc->num_big = bpos;  // all big tiles (the list's consumers reset it)
   }
   // the last CTA to finish leaves the look-back state zero for the next call
   __syncthreads();
@@ -560,7 +575,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(
     if (threadIdx.x == 0) {
       ctl->ticket = 0u;
       ctl->done = 0u;
-      sc->num_small = 0u;
     }
   }
 }
