@@ -2693,7 +2693,8 @@ struct BwdIn {
 
 template <int CMAX>
 struct PixBwd {
-  float T, GA, GD, S, SD, P;  // S = G . R (R: everything behind, normalised), SD likewise for depth
+  float T, GA, GD, S, SD, P;  // S = G . R (R: everything behind, normalised), SD likewise for depth;
+                              // default build: S holds the unnormalised Q (bwd_pixel), SD / P unused
   float G[CMAX];
   uint32_t last;
 };
@@ -2738,6 +2739,11 @@ __device__ __forceinline__ void load_pixel_bwd(const DevCam& cam, const DevCfg& 
         if (c < g.C) s.S += s.G[c] * b[c];
     }
   }
+#ifndef INPC_BWD_NORMALISED
+  // unnormalised accumulator of everything behind the current fragment:
+  // Q = T_final (G . bg - G_A), grown by T_k alpha_k (G . f_k + G_D z_k)
+  s.S = s.T * (s.S - s.GA);
+#endif
 #pragma unroll
   for (int c = 0; c < CMAX; ++c) Gs[c] = s.G[c];
 }
@@ -2789,7 +2795,16 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
 #pragma unroll
       for (int c = 0; c < CMAX; ++c) gf += s.G[c] * cs.f[e][c];
     }
+#ifdef INPC_BWD_NORMALISED
     const float dA = Tk * ((gf - s.S) + s.GD * (z - s.SD) + s.GA * s.P);
+#else
+    // Eq. 2 with the behind-terms unnormalised: T_k S_k = B_k / (1 - alpha_k),
+    // T_k SD_k = BD_k / (1 - alpha_k), T_k P_k = T_final / (1 - alpha_k), so
+    // dL/dalpha_k = T_k (G.f_k + G_D z_k) - Q_k / (1 - alpha_k) with
+    // Q_k = B_k + G_D BD_k - G_A T_final (one running sum instead of three)
+    const float h = fmaf(s.GD, z, gf);
+    const float dA = fmaf(-s.S, rcp, Tk * h);
+#endif
     const float ta = Tk * alpha;
     const float go = gw * dA;  // dalpha/do = w, or 0 where the clamp is active
     if (SM::kSlots) {
@@ -2800,9 +2815,13 @@ __device__ __forceinline__ void bwd_pixel(BwdSmem<MODE, CMAX>& S, const DevCfg& 
         if (c < g.C) atomicAdd(&S.acc[e][c], ta * s.G[c]);
       atomicAdd(&S.acc[e][CMAX], go);
     }
+#ifdef INPC_BWD_NORMALISED
     s.S = alpha * gf + one_m * s.S;
     s.SD = alpha * z + one_m * s.SD;
     s.P *= one_m;
+#else
+    s.S = fmaf(ta, h, s.S);
+#endif
     s.T = Tk;
   }
 }
