@@ -76,7 +76,8 @@ def kernel_bytes(N, Nv, Ft, P, C, sh=False, env=False, F_mid=0, F_huge=0):
     """Compulsory bytes per kernel, for the roofline of the
     dominant kernel only -- NOT summed into the step (bin_fused is the sum of
     project_count and scatter; the step model is step_bytes_survey).
-    F_mid / F_huge: entries of tiles of 257..2048 / over 2048 entries, which
+    F_mid / F_huge: entries of tiles of 257..mid_max / over mid_max entries (mid_max
+    = 2048, or 8192 where the 8192 merge class runs), which
     the mid / big-tile sorts read once (8-byte key) and write once (4-byte
     index)."""
     fbytes = (36 if sh else 4) * C
@@ -416,13 +417,18 @@ def run_ours(args, rank, world, local_rank):
     dbg = inpc.make_cfg(H, W, C, mode, flags=flags | inpc.FLAG_DEBUG, env_hw=env_hw)
     ctx.forward(dbg, cams, xyz, feat, op, bg=env_t)
     Nv = Ft = F_mid = F_huge = 0
+    # the merge sort's largest class: 8192 entries on dense clouds (the
+    # library's rule, N >= 512 tiles; INPC_MERGE8K forces it), else 2048
+    n_tiles = ((W + 7) // 8) * ((H + 7) // 8)
+    m8 = os.environ.get("INPC_MERGE8K")
+    mid_max = 8192 if (m8 == "1" or (m8 != "0" and N >= 512 * n_tiles)) else 2048
     for v in range(V):
         ex = ctx.debug_export(v, N=N, H=H, W=W)
         Nv += int((ex["tiles_touched"] > 0).sum().item())
         Ft += int(ex["F_t"])
         cnt = ex["tile_ranges"][1:].long() - ex["tile_ranges"][:-1].long()
-        F_mid += int(cnt[(cnt > 256) & (cnt <= 2048)].sum().item())
-        F_huge += int(cnt[cnt > 2048].sum().item())
+        F_mid += int(cnt[(cnt > 256) & (cnt <= mid_max)].sum().item())
+        F_huge += int(cnt[cnt > mid_max].sum().item())
     sh, env = "sh" in args.variant, "env" in args.variant
     kmodel = kernel_bytes(N * V, Nv, Ft, P * V, C, sh=sh, env=env, F_mid=F_mid, F_huge=F_huge)
     step_bytes = step_bytes_survey(N * V, Nv, Ft, P * V, C, fwd_only, sh=sh, env=env)
@@ -616,7 +622,7 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config], "variant": args.variant, "N": N,
                        "views_per_step": wl["frames_per_step"], "views_per_rank": V,
-                       "N_visible": Nv, "F_t": Ft, "F_mid": F_mid, "F_huge": F_huge, "H": H, "W": W,
+                       "N_visible": Nv, "F_t": Ft, "F_mid": F_mid, "F_huge": F_huge, "F_mid_max": mid_max, "H": H, "W": W,
                        "C": C, "mode": mode, "alpha_max": 0.99, "t_min": 1e-4,
                        "point_order": order, "parallelism": wl["parallelism"],
                        "l2": "flushed: 256 MiB write between steps, outside the per-step events"},
