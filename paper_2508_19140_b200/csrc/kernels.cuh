@@ -1942,9 +1942,9 @@ __global__ void __launch_bounds__(NT) k_sort_mid_merge(
     const int np = NT * q;
     uint32_t* srcb = buf0;
     uint32_t* dstb = buf1;
-    for (int L = q; L < np; L <<= 1) {
+    for (int L = q, ps = 1; L < np; L <<= 1, ++ps) {
       const int o0 = tid * q;
-      const int P = o0 / (2 * L) * (2 * L);  // 2L = q 2^(p+1), q odd
+      const int P = (tid >> ps) * (2 * L);  // o0 / 2L with 2L = q 2^ps: no integer division
       const int d = o0 - P;
       int lo = d > L ? d - L : 0, hi = d < L ? d : L;
       while (lo < hi) {
