@@ -1052,7 +1052,14 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
       o.T_final = (float*)vs.T_final.p;
       o.last = (uint32_t*)vs.last.p;
       o.order = vs.has_order ? (const uint32_t*)vs.order.p : nullptr;
-      const bool pf = N < kFwdPrefetchMaxDensity * (int64_t)T;
+      static const int pf_env = [] {  // INPC_FWD_PF=0 / 1 forces the choice (A/B)
+        const char* e = getenv("INPC_FWD_PF");
+        return e ? atoi(e) : -1;
+      }();
+      // record prefetch: always with the 16-byte records (cfg 4: 1.613 -> 1.566 ms;
+      // its 32-byte records were faster without, 514 vs 780 us in round 1), else
+      // for clouds below the density bound
+      const bool pf = pf_env >= 0 ? pf_env == 1 : (rec16 || N < kFwdPrefetchMaxDensity * (int64_t)T);
       if (gauss)
         dispatch_blend_fwd<1>(cmax, band_tiles, sv, dc, g, (const PointRec*)vs.rec.p, feat_blend, false, bg_v,
                               (const uint32_t*)vs.ranges.p, (const unsigned long long*)X.entries.p,
