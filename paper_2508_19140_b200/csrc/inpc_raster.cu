@@ -574,8 +574,8 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
     int o1 = 0, o2 = 0, o3 = 0;
     cudaFuncSetAttribute(k_sort_mid_merge<512, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)MidMerge<512, 8192>::kSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_sort_mid_merge<64, 1024>, 64, MidMerge<64, 1024>::kSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_sort_mid_merge<128, 2048>, 128, MidMerge<128, 2048>::kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_sort_mid_merge<kMidNT1, 1024>, kMidNT1, MidMerge<kMidNT1, 1024>::kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_sort_mid_merge<kMidNT2, 2048>, kMidNT2, MidMerge<kMidNT2, 2048>::kSmem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_sort_mid_merge<512, 8192>, 512, MidMerge<512, 8192>::kSmem);
     c->midw_grid[2] = c->num_sms * (o3 > 0 ? o3 : 1);
     c->midw_grid[0] = c->num_sms * (o1 > 0 ? o1 : 1);
@@ -1001,10 +1001,10 @@ int inpc_rasterize_fwd(inpc_ctx* c, const inpc_raster_cfg* cfg, const inpc_camer
         uint32_t* dn = (uint32_t*)X.overflow.p + 6;
         uint32_t* l2 = (uint32_t*)X.mid_l2.p;
         uint32_t* l3 = (uint32_t*)X.mid_l3.p;
-        k_sort_mid_merge<64, 1024><<<c->midw_grid[0], 64, MidMerge<64, 1024>::kSmem, sv>>>(
+        k_sort_mid_merge<kMidNT1, 1024><<<c->midw_grid[0], kMidNT1, MidMerge<kMidNT1, 1024>::kSmem, sv>>>(
             rp, bp, &sc->num_big, &sc->max_big, ep, sp, l2, &sc->num_l2, dn);
         CK(cudaGetLastError());
-        k_sort_mid_merge<128, 2048><<<c->midw_grid[1], 128, MidMerge<128, 2048>::kSmem, sv>>>(
+        k_sort_mid_merge<kMidNT2, 2048><<<c->midw_grid[1], kMidNT2, MidMerge<kMidNT2, 2048>::kSmem, sv>>>(
             rp, l2, &sc->num_l2, nullptr, ep, sp, merge8k ? l3 : nullptr, &sc->num_l3, dn + 1);
         CK(cudaGetLastError());
         if (merge8k)

@@ -1569,7 +1569,15 @@ struct MidSort {
 };
 constexpr int kMidThreads = 128;
 constexpr int kMidMax = 2048;
-constexpr int kMergeMax = 8192;  // k_sort_mid_merge's largest tiles; k_sort_big takes the rest
+constexpr int kMergeMax = 8192;
+#ifndef INPC_MID_NT1
+#define INPC_MID_NT1 64
+#endif
+#ifndef INPC_MID_NT2
+#define INPC_MID_NT2 128
+#endif
+constexpr int kMidNT1 = INPC_MID_NT1;  // merge-sort threads per tile of <= 1024 entries
+constexpr int kMidNT2 = INPC_MID_NT2;  // ... of <= 2048 entries  // k_sort_mid_merge's largest tiles; k_sort_big takes the rest
 using MidCfg = MidSort<kMidThreads, kMidMax>;
 
 // Sort the n keys of S.s (slot order); returns true with S.k32 holding the
