@@ -563,6 +563,17 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
   cudaFuncSetAttribute(k_sort_big, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_big, kBigThreadsLarge, big_smem);
   c->big_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
+  {
+    // k_sort_big is launched for every unfused view and mostly finds its list
+    // empty: a cooperative grid of every resident CTA must wait for whole SMs
+    // while the other view streams' kernels run (cfg 5: 37.4 ms per step with
+    // 296 CTAs, 36.3 with 32, 36.2 with 16).  32 CTAs still sort the rare huge
+    // tiles (dense clouds send their 2049-8192-entry tiles to the merge sort).
+    // env INPC_BIG_GRID: CTAs, 0 = every resident CTA (A/B)
+    const char* e = getenv("INPC_BIG_GRID");
+    const int want = e ? atoi(e) : 32;
+    if (want > 0 && want < c->big_grid) c->big_grid = want;
+  }
   per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_mid, kMidThreads, 0);
   c->mid_grid = c->num_sms * (per_sm > 0 ? per_sm : 1);
