@@ -99,11 +99,11 @@ struct inpc_ctx {
   const float* chunk_xyz = nullptr;
   int64_t chunk_N = 0;
   // scratch: two sets (views alternate between the two internal streams)
-  static constexpr int kMaxViewStreams = 4;
+  static constexpr int kMaxViewStreams = 8;
   Scratch scr[kMaxViewStreams];
   cudaStream_t vstream[kMaxViewStreams] = {};  // internal non-blocking streams for multi-view calls
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxViewStreams] = {};
-  int view_streams = 4;                        // env INPC_VIEW_STREAMS (1 = one stream, A/B)
+  int view_streams = 8;                        // env INPC_VIEW_STREAMS (1 = one stream, A/B)
   Buf det_f, det_o;  // deterministic gradients: per-entry sums at list positions
   Buf f4_rec, f4_keys, f4_vals, f4_keys2, f4_vals2, f4_hist, f4_scan, f4_misc;  // NEXT f4 baseline
   int bin_grid[3] = {0, 0, 0};  // cooperative grid of k_bin_bilinear<2,4,8>
@@ -616,7 +616,7 @@ int inpc_ctx_create(inpc_ctx** out, int device) {
   }
   {
     const char* e = getenv("INPC_VIEW_STREAMS");
-    c->view_streams = e ? atoi(e) : 4;  // 4 vs 2: 37.0 vs 37.5 ms per cfg 5 step (round-2 end)
+    c->view_streams = e ? atoi(e) : 8;  // cfg 5 step: 2 / 4 / 6 / 8 streams 36.8 / 36.3 / 36.16 / 36.09 ms (round-2 end)
     if (c->view_streams < 1) c->view_streams = 1;
     if (c->view_streams > inpc_ctx::kMaxViewStreams) c->view_streams = inpc_ctx::kMaxViewStreams;
   }
